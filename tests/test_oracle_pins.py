@@ -1,0 +1,319 @@
+"""Pins for the oracle: each check ties oracle/ to something other than itself
+(hand-computed values, published KATs, closed forms, brute force through a
+different library routine, invariants).  CPU only."""
+import json
+import math
+import os
+import struct
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import bank_corpus, init_rows, uniform_matrix
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _bits(a):
+    return [f"{struct.unpack('<I', struct.pack('<f', float(v)))[0]:08x}" for v in np.ravel(a)]
+
+
+def _rn_f32(q: Fraction) -> np.float32:
+    """Exact round-to-nearest-even of a rational to binary32 (normal range)."""
+    if q == 0:
+        return np.float32(0.0)
+    sign = -1 if q < 0 else 1
+    q = abs(q)
+    e = math.floor(math.log2(q.numerator) - math.log2(q.denominator))
+    while Fraction(2) ** e > q:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= q:
+        e += 1
+    scaled = q / Fraction(2) ** (e - 23)          # in [2^23, 2^24)
+    m = math.floor(scaled)
+    rem = scaled - m
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and m % 2 == 1):
+        m += 1
+    return np.float32(sign * m * 2.0 ** (e - 23))
+
+
+# ------------------------------------------------------------------ sampler
+def test_splitmix64_published_kat():
+    g = _gold("splitmix64_kat.json")
+    got = [f"{oracle.splitmix64(0, t):016x}" for t in range(3)]
+    assert got == g["seed0_first3"]
+
+
+def test_sample_index_survey_regression_and_range():
+    g = _gold("splitmix64_kat.json")
+    assert [oracle.sample_index(1, t, 200) for t in range(10)] == g["survey_A9_seed1_n200_i0_9"]
+    assert [oracle.sample_index(42, t, 5000) for t in range(10)] == g["survey_A9_seed42_n5000_i0_9"]
+    idx = np.array([oracle.sample_index(7, t, 13) for t in range(20000)])
+    assert idx.min() == 0 and idx.max() == 12
+    # uniform with replacement (R8): chi-square-ish sanity, 13 bins
+    cnt = np.bincount(idx, minlength=13)
+    assert np.all(np.abs(cnt - 20000 / 13) < 5 * math.sqrt(20000 / 13))
+
+
+# ----------------------------------------------------------------- schedule
+def test_schedule_endpoints_closed_form():
+    a0, s0 = 0.1, 5.0
+    a, s, r2 = oracle.schedule(0, 2000, a0, s0)
+    assert a == a0 and s == s0                          # alpha_0 = alpha0 exactly (R6)
+    assert math.isclose(r2, 2 * 25 * math.log(1e4), rel_tol=1e-15)
+    # alpha(T-1) / (alpha0/100) = exp(ln100 (1 - ((T-1)/T)^2)): 1.0046 at T=2000 (SURVEY [A2])
+    a, _, _ = oracle.schedule(1999, 2000, a0, s0)
+    assert abs(a / (a0 / 100) - 1.0046) < 1e-4
+    a, _, _ = oracle.schedule(499999, 500000, a0, s0)
+    assert abs(a / (a0 / 100) - 1.0000184) < 1e-6
+    # sigma floor (R3): sigma0 = 0.5 is floored to sigma_min = 1
+    _, s, _ = oracle.schedule(0, 10, 0.1, 0.5)
+    assert s == 1.0
+    # eps = 0 -> no cutoff
+    _, _, r2 = oracle.schedule(3, 10, 0.1, 2.0, eps=0.0)
+    assert r2 == math.inf
+    # monotone non-increasing in t for all three decay kinds, all end at 1 %
+    for kind in (0, 1, 2):
+        al = [oracle.schedule(t, 100, 1.0, 10.0, kind=kind)[0] for t in range(101)]
+        assert all(x >= y for x, y in zip(al, al[1:]))
+        assert math.isclose(al[-1], 0.01, rel_tol=1e-12)
+
+
+# ------------------------------------------------------------------ lattice
+def test_lattice_spec_examples():
+    g = _gold("lattice.json")
+    cols = 7
+    for (iu, ju), (iv, jv), want in g["hex_pairs_g2"]:
+        assert oracle.lattice_g2(6, cols, 1, iu * cols + ju, iv * cols + jv) == want
+    for (iu, ju), (iv, jv), want in g["rect_pairs_g2"]:
+        assert oracle.lattice_g2(6, cols, 0, iu * cols + ju, iv * cols + jv) == want
+
+
+def test_lattice_symmetry_and_spec_positions():
+    rows, cols = 6, 7
+    N = rows * cols
+    for topo in (0, 1):
+        for u in range(N):
+            for v in range(N):
+                g = oracle.lattice_g2(rows, cols, topo, u, v)
+                assert g == oracle.lattice_g2(rows, cols, topo, v, u)
+                assert g * 4 == int(g * 4)                  # multiples of 1/4: exact
+                # SPEC S:164 planar positions, evaluated independently in float
+                iu, ju, iv, jv = u // cols, u % cols, v // cols, v % cols
+                if topo == 1:
+                    pu = (ju + 0.5 * (iu % 2), iu * math.sqrt(3) / 2)
+                    pv = (jv + 0.5 * (iv % 2), iv * math.sqrt(3) / 2)
+                else:
+                    pu, pv = (ju, iu), (jv, iv)
+                ref = (pu[0] - pv[0]) ** 2 + (pu[1] - pv[1]) ** 2
+                assert abs(g - ref) < 1e-12
+
+
+def test_hex_neighbour_histogram():
+    g = _gold("lattice.json")
+    rows, cols = 6, 7
+    hist = {}
+    for u in range(rows * cols):
+        c = sum(oracle.lattice_g2(rows, cols, 1, u, v) == 1.0 for v in range(rows * cols))
+        hist[str(c)] = hist.get(str(c), 0) + 1
+    assert hist == g["hex_6x7_neighbour_histogram"]
+    # rectangular: interior units have exactly 4
+    c = sum(oracle.lattice_g2(6, 7, 0, 2 * 7 + 3, v) == 1.0 for v in range(42))
+    assert c == 4
+
+
+# ----------------------------------------------------- worked example (Eq. 1)
+@pytest.mark.parametrize("topo,key", [(0, "rect"), (1, "hex")])
+def test_worked_example_2x2(topo, key):
+    g = _gold("worked_example_2x2.json")
+    W = np.array(g["W"], np.float32)
+    x = np.array(g["x"], np.float32)
+    c, D, _ = oracle.bmu(W, x)
+    assert c == g["bmu"] and D == np.float32(g["D2"][c])
+    W1 = oracle.update(W.copy(), 2, 2, topo, x, c, g["alpha"], g["sigma"], math.inf)
+    assert _bits(W1) == [b for row in g[key]["W_new_bits"] for b in row]
+    # independent derivation: exact rational evaluation of fmaf(h, RN(x-w), w)
+    for u in range(4):
+        g2 = g[key]["g2"][u]
+        assert oracle.lattice_g2(2, 2, topo, u, c) == g2
+        h = np.float32(g["alpha"] * math.exp(-g2 / 2.0))
+        if key == "rect":
+            assert abs(float(h) - g["rect"]["h"][u]) < 1e-9
+        for k in range(2):
+            diff = _rn_f32(Fraction(float(x[k])) - Fraction(float(W[u, k])))
+            want = _rn_f32(Fraction(float(h)) * Fraction(float(diff)) + Fraction(float(W[u, k])))
+            assert W1[u, k] == want
+    U = oracle.umatrix(W, 2, 2, topo)
+    np.testing.assert_allclose(U, g[key]["U"], rtol=0, atol=1e-7)
+
+
+def test_tie_rule():
+    g = _gold("worked_example_2x2.json")
+    W = np.array(g["W"], np.float32)
+    c, D, m = oracle.bmu(W, np.array(g["tie"]["x_all_equal"], np.float32))
+    assert c == g["tie"]["bmu_all_equal"] and m == 0.0
+    b1, b2, d1 = oracle.map_docs(W, np.array([g["tie"]["map_x"]], np.float32))
+    assert (b1[0], b2[0]) == (g["tie"]["map_bmu1"], g["tie"]["map_bmu2"])
+    # rect: 1 and 0 adjacent -> TE contribution 0
+    assert oracle.topographic_error_from_bmus(2, 2, 0, b1, b2) == 0.0
+
+
+def test_spec_update_examples():
+    # 1-unit map, alpha = 0.1 at t = 0: w = (0), x = (1) -> w' = (0.1)
+    W = np.zeros((1, 1), np.float32)
+    W1, log = oracle.train_online(W, 1, 1, 0, np.ones((1, 1), np.float32), epochs=1,
+                                  alpha0=0.1, sigma0=1.0, seed=3)
+    assert W1[0, 0] == np.float32(0.1) and log[0] == 0
+    # S:213 h = 0 -> unchanged; alpha = 0 here
+    W = uniform_matrix(4, 5, 1)
+    W1 = oracle.update(W.copy(), 2, 2, 0, uniform_matrix(1, 5, 2)[0], 0, 0.0, 1.0, math.inf)
+    assert np.array_equal(W1, W)
+
+
+# -------------------------------------------------------------- BMU / map
+def test_bmu_and_map_brute_force():
+    for seed in range(5):
+        W = uniform_matrix(23, 17, seed)
+        X = uniform_matrix(40, 17, 100 + seed)
+        b1, b2, d1, m12, _ = oracle.map_docs(W, X, want_margins=True)
+        for i in range(40):
+            # different summation (numpy pairwise) in fp64, then fp32 key (R9, R10)
+            acc = np.sum((X[i].astype(np.float64) - W.astype(np.float64)) ** 2, axis=1)
+            D = acc.astype(np.float32)
+            order = np.lexsort((np.arange(23), D))
+            assert b1[i] == order[0] and b2[i] == order[1]
+            assert d1[i] == D[order[0]]
+            c, Dc, _ = oracle.bmu(W, X[i])
+            assert c == order[0] and Dc == D[order[0]]
+
+
+def test_map_csr_identity_matches_dense():
+    C = bank_corpus(150, 400, seed=5)
+    X = C.dense()
+    W = init_rows(X, 30, 9) * np.float32(0.5) + np.float32(0.01)
+    a = oracle.map_docs(W, X)
+    b = oracle.map_docs_csr(W, C.indptr, C.indices, C.data)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    np.testing.assert_allclose(a[2], b[2], rtol=2e-7, atol=0)
+
+
+def test_qerror_spec_examples():
+    # S:230 single prototype equal to every row -> 0
+    X = np.tile(uniform_matrix(1, 6, 3), (5, 1))
+    assert oracle.qerror(X[:1], X) == 0.0
+    # S:231 unit-norm rows, single zero prototype -> 1.0
+    C = bank_corpus(50, 100, seed=1)
+    assert abs(oracle.qerror(np.zeros((1, 100), np.float32), C.dense()) - 1.0) < 1e-6
+    # S:232 rows {(0),(2)}, one prototype (1) -> 1.0
+    assert oracle.qerror(np.array([[1.0]], np.float32), np.array([[0.0], [2.0]], np.float32)) == 1.0
+
+
+def test_one_unit_map_degenerate():
+    X = uniform_matrix(10, 4, 0)
+    W1, log = oracle.train_online(X[:1], 1, 1, 1, X, epochs=2, alpha0=0.1, sigma0=0.5, seed=1)
+    assert np.all(log == 0)
+    assert oracle.topographic_error(W1, 1, 1, 1, X) == 0.0
+    assert oracle.umatrix(W1, 1, 1, 1)[0] == 0.0
+
+
+# ---------------------------------------------------------------- invariants
+def test_zero_rate_leaves_weights_bit_identical():
+    C = bank_corpus(60, 80, seed=2)
+    X = C.dense()
+    W0 = init_rows(X, 12, 2)
+    W1, _ = oracle.train_online(W0, 3, 4, 1, X, epochs=3, alpha0=0.0, sigma0=2.0, seed=4)
+    assert np.array_equal(W1, W0)
+
+
+def test_t_range_resume_is_exact():
+    C = bank_corpus(50, 60, seed=3)
+    X = C.dense()
+    W0 = init_rows(X, 9, 3)
+    Wa, la = oracle.train_online(W0, 3, 3, 1, X, epochs=4, alpha0=0.1, sigma0=1.5, seed=11)
+    Wb, lb1 = oracle.train_online(W0, 3, 3, 1, X, epochs=4, alpha0=0.1, sigma0=1.5, seed=11,
+                                  t_begin=0, t_end=77)
+    Wb, lb2 = oracle.train_online(Wb, 3, 3, 1, X, epochs=4, alpha0=0.1, sigma0=1.5, seed=11,
+                                  t_begin=77, t_end=-1)
+    assert np.array_equal(Wa, Wb) and np.array_equal(la, np.concatenate([lb1, lb2]))
+
+
+def test_thread_count_invariance():
+    C = bank_corpus(100, 3000, seed=4)
+    X = C.dense()
+    W0 = init_rows(X, 100, 4)
+    nt = oracle.num_threads()
+    try:
+        oracle.set_num_threads(1)
+        W1, l1 = oracle.train_online(W0, 10, 10, 1, X, epochs=1, alpha0=0.1, sigma0=5, seed=2)
+        oracle.set_num_threads(max(nt, 4))
+        W2, l2 = oracle.train_online(W0, 10, 10, 1, X, epochs=1, alpha0=0.1, sigma0=5, seed=2)
+    finally:
+        oracle.set_num_threads(nt)
+    assert np.array_equal(W1, W2) and np.array_equal(l1, l2)
+
+
+def test_eq1_contraction_and_convex_hull():
+    # S:244 |x - w'| = (1 - h)|x - w| (up to fp32 rounding); S:247 convex hull
+    rng = np.random.default_rng(0)
+    W = rng.uniform(0, 1, (6, 9)).astype(np.float32)
+    x = rng.uniform(0, 1, 9).astype(np.float32)
+    W1 = oracle.update(W.copy(), 2, 3, 1, x, 4, 0.3, 1.2, math.inf)
+    for u in range(6):
+        g2 = oracle.lattice_g2(2, 3, 1, u, 4)
+        h = float(np.float32(0.3 * math.exp(-g2 / (2 * 1.2 * 1.2))))
+        np.testing.assert_allclose(np.abs(x - W1[u]), (1 - h) * np.abs(x - W[u]), atol=3e-7)
+    C = bank_corpus(80, 50, seed=6)
+    X = C.dense()
+    W0 = init_rows(X, 16, 6)
+    Wf, _ = oracle.train_online(W0, 4, 4, 1, X, epochs=5, alpha0=0.5, sigma0=2.0, seed=1)
+    lo = np.minimum(X.min(0), W0.min(0))
+    hi = np.maximum(X.max(0), W0.max(0))
+    assert np.all(Wf >= lo - 1e-6) and np.all(Wf <= hi + 1e-6)
+
+
+def test_fixed_point_identical_rows():
+    # k identical rows, long schedule -> QE -> 0 within 1e-3
+    row = uniform_matrix(1, 40, 8)
+    X = np.tile(row, (7, 1))
+    W0 = uniform_matrix(9, 40, 5) * np.float32(0.2)
+    Wf, _ = oracle.train_online(W0, 3, 3, 1, X, epochs=300, alpha0=0.5, sigma0=1.5, seed=5, eps=0.0)
+    assert oracle.qerror(Wf, X) <= 1e-3
+
+
+def test_topology_preservation_three_clusters():
+    # SPEC acceptance 5: intra-cluster BMU grid distance < inter
+    wins = 0
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        centers = rng.uniform(0, 1, (3, 30)) * 4
+        X = np.concatenate([c + 0.05 * rng.standard_normal((100, 30)) for c in centers]).astype(np.float32)
+        lab = np.repeat(np.arange(3), 100)
+        W0 = init_rows(X, 36, seed)
+        Wf, _ = oracle.train_online(W0, 6, 6, 1, X, epochs=5, alpha0=0.1, sigma0=3.0, seed=seed)
+        b1, _, _ = oracle.map_docs(Wf, X)
+        sub = rng.choice(300, 90, replace=False)
+        intra, inter = [], []
+        for a in sub:
+            for b in sub:
+                if a < b:
+                    g = math.sqrt(oracle.lattice_g2(6, 6, 1, b1[a], b1[b]))
+                    (intra if lab[a] == lab[b] else inter).append(g)
+        wins += np.mean(intra) < np.mean(inter)
+    assert wins >= 9
+
+
+def test_qe_improves_on_bank_corpus():
+    # SPEC acceptance 6: final QE <= 0.8 x initial QE
+    C = bank_corpus(200, 500, seed=1)
+    X = C.dense()
+    W0 = uniform_matrix(100, 500, 1) * np.float32(0.1)   # random initial codebook
+    q0 = oracle.qerror(W0, X)
+    Wf, _ = oracle.train_online(W0, 10, 10, 0, X, epochs=10, alpha0=0.1, sigma0=5.0, seed=1)
+    assert oracle.qerror(Wf, X) <= 0.8 * q0
