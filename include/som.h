@@ -1,0 +1,170 @@
+/*
+ * som.h — C ABI of libsom, the B200 (sm_100a) implementation of the CUDASOM
+ * hot path (Gavval et al., arXiv 1905.09598): online Kohonen SOM training
+ * (distance -> argmin BMU -> Gaussian-neighbourhood update, Eq. 1), batch
+ * BMU mapping, quantization / topographic error and the U-matrix.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Rn = reading n in
+ * DESIGN.md §3 (where the paper is silent, ambiguous or garbled).
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Plain C: no C++ types, no exceptions, no torch types.  Every call
+ *    returns a som_status; SOM_OK = 0.  A human-readable message for the
+ *    last failure on the calling thread is returned by som_last_error().
+ *  - Ownership: the handle owns the map W (rows*cols x dim fp32, row-major,
+ *    unit u = i*cols + j) and all device scratch.  Inputs X and
+ *    all outputs are caller-owned and may be HOST or DEVICE pointers (device
+ *    memory of the handle's device; detected per pointer).  Host buffers are
+ *    staged through device scratch inside the call.  The library keeps no
+ *    caller pointer after a call returns.
+ *  - Layout: X is n x dim fp32 row-major (one L2-normalised TF-IDF document
+ *    per row).  CSR inputs use int64 rowptr[n+1], int32
+ *    col[nnz] and fp32 val[nnz].
+ *  - Synchrony: calls run on the handle's stream (som_set_stream; default a
+ *    stream the handle creates) and return after that work completes.
+ *  - Validation happens before any side effect: SOM_EINVAL for bad sizes or
+ *    parameters, SOM_EEMPTY for n = 0 where data is required.
+ *  - A CUDA failure returns SOM_ECUDA and poisons the handle: every later
+ *    call except som_destroy returns SOM_ESTATE.
+ *  - Thread safety: one handle must not be used concurrently; distinct
+ *    handles are independent.
+ *  - Determinism: identical inputs and seed give bit-identical W, BMU log
+ *    and mapping outputs on every run.
+ *  - There is no CPU fallback: without a usable sm_100a device som_create
+ *    fails with SOM_ECUDA.
+ */
+#ifndef SOM_H
+#define SOM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct som_ctx som_ctx; /* opaque handle */
+
+typedef enum {
+    SOM_OK = 0,
+    SOM_EINVAL = 1,      /* bad size / parameter / t-range                     */
+    SOM_EDIM = 2,        /* dimension mismatch                 */
+    SOM_EEMPTY = 3,      /* n = 0 where data is required              */
+    SOM_ENOMEM = 4,      /* device or host allocation failed                  */
+    SOM_ECUDA = 5,       /* CUDA runtime/launch failure (handle poisoned)     */
+    SOM_ENCCL = 6,       /* NCCL failure (handle poisoned)                    */
+    SOM_ESTATE = 7,      /* handle poisoned by an earlier failure             */
+    SOM_EUNSUPPORTED = 8 /* valid request this build/device cannot serve      */
+} som_status;
+
+typedef enum { SOM_RECT = 0, SOM_HEX = 1 } som_topology; /* P:166 hex; rect BJ:7 */
+
+typedef enum {
+    SOM_DECAY_GAUSSIAN = 0, /* f = exp(-k tau^2)   (R1, "Gaussian decay") */
+    SOM_DECAY_LINEAR = 1,   /* f = 1 - (1 - e^-k) tau                          */
+    SOM_DECAY_EXP = 2       /* f = exp(-k tau)                                 */
+} som_decay_kind;
+
+/* Decay schedule (R1-R6): tau = t/T, alpha_t = alpha0 f,
+ * sigma_t = max(sigma_min, sigma0 f); only units with lattice distance^2
+ * g2 <= 2 sigma_t^2 ln(1/cutoff) adapt (R5; cutoff = 0: every unit). */
+typedef struct {
+    int32_t kind;      /* som_decay_kind; default SOM_DECAY_GAUSSIAN */
+    double k;          /* decay constant; default ln(100)            */
+    double sigma_min;  /* radius floor; default 1.0 (R3)              */
+    double cutoff;     /* epsilon; default 1e-4 (R5); 0 = no cutoff  */
+} som_schedule;
+
+typedef enum {
+    SOM_MAP_AUTO = 0,      /* fastest path available on the device          */
+    SOM_MAP_EXACT_F64 = 1, /* fp64-accumulated direct distances (= oracle)   */
+    SOM_MAP_3XTF32 = 2     /* tcgen05 3xTF32 GEMM |x|^2 - 2 x.w + |w|^2 (R20) */
+} som_map_precision;
+
+/* Fill *s with the defaults above. */
+som_status som_schedule_default(som_schedule *s);
+
+/* Create a rows x cols map of dim-dimensional prototypes on CUDA device
+ * `device` ("a three dimensional data structure is used to represent
+ * the map along with its weight vectors", flattened).  Weights start at 0.
+ * rows, cols, dim >= 1; rows*cols < 2^24; topology in som_topology. */
+som_status som_create(int32_t rows, int32_t cols, int32_t dim, int32_t topology,
+                      int32_t device, som_ctx **out);
+void som_destroy(som_ctx *h);
+
+/* Copy N*dim fp32 weights in (set) / out (get).  Host or device pointer. */
+som_status som_set_weights(som_ctx *h, const float *w);
+som_status som_get_weights(som_ctx *h, float *w);
+
+/* Seeded initial codebook: the rows X[j_0..j_{N-1}] with the j drawn from
+ * SplitMix64(seed) without replacement when N <= n, with replacement
+ * otherwise (R18; the paper's PCA-plane init, is NEXT-3). */
+som_status som_init_random(som_ctx *h, const float *X, int64_t n, uint64_t seed);
+
+/* Online ("standard") SOM training: for each step
+ * t in [t_begin, t_end) of T = epochs * n steps (R7):
+ *   i_t   = sample index: t-th SplitMix64(seed) output mapped to [0,n) (R8)
+ *   c_t   = argmin_u (RN_fp32(sum_k (x_k - w_uk)^2 in fp64), u)  (R9, R10)
+ *   w_u  <- fmaf(h_u, x - w_u, w_u) for units within the cutoff   (Eq. 1, R11)
+ *   h_u   = RN_fp32(alpha_t exp(-g2(u,c_t) / (2 sigma_t^2)))      (R4)
+ * t_end = -1 means T.  epochs = 0 is a valid no-op.  bmu_log
+ * (nullable, host or device, t_end - t_begin int32) receives c_t.
+ * Resuming with a later t-range continues bit-exactly.  alpha0 in [0,1],
+ * sigma0 > 0; s may be NULL (defaults). */
+som_status som_train_online(som_ctx *h, const float *X, int64_t n, int32_t epochs,
+                            double alpha0, double sigma0, const som_schedule *s,
+                            uint64_t seed, int64_t t_begin, int64_t t_end,
+                            int32_t *bmu_log);
+
+/* Where som_train_online keeps each CTA's prototypes between steps:
+ * AUTO picks shared memory when a CTA's share of W fits (else global
+ * memory, L2-resident when W fits the L2).  Forcing SHARED for a map that
+ * does not fit returns SOM_EUNSUPPORTED from som_train_online. */
+typedef enum { SOM_TRAIN_AUTO = 0, SOM_TRAIN_W_SHARED = 1, SOM_TRAIN_W_GLOBAL = 2 } som_train_mode;
+som_status som_set_train_mode(som_ctx *h, int32_t mode);
+
+/* Batch mapping ("assigned each document vector to the best matching
+ * vector on the trained map"): for each row, bmu1 = argmin (D,u),
+ * bmu2 = argmin over u != bmu1 (-1 if N = 1), d2 = D at bmu1 (squared
+ * Euclidean, fp32).  bmu2, d2 nullable.  Precision per som_set_map_precision. */
+som_status som_map(som_ctx *h, const float *X, int64_t n, int32_t *bmu1, int32_t *bmu2,
+                   float *d2);
+som_status som_map_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
+                       const float *val, int64_t n, int32_t *bmu1, int32_t *bmu2,
+                       float *d2);
+som_status som_set_map_precision(som_ctx *h, int32_t precision);
+
+/* Quantization error (R14; Table 2): mean over rows of
+ * sqrt(D at the BMU), summed in fp64.  n >= 1. */
+som_status som_qerror(som_ctx *h, const float *X, int64_t n, double *qe);
+/* Topographic error (R15; BJ:5): fraction of rows whose two best units are
+ * not lattice-adjacent (g2 != 1; 0 for a 1-unit map).  n >= 1. */
+som_status som_topographic_error(som_ctx *h, const float *X, int64_t n, double *te);
+/* Both errors from one mapping pass. */
+som_status som_errors(som_ctx *h, const float *X, int64_t n, double *qe, double *te);
+
+/* U-matrix (R16; BJ:5): U_u = mean over lattice-adjacent v (g2 = 1) of
+ * |w_u - w_v|_2 (fp64 accumulation, fp32 result), 0 with no neighbour.
+ * U: N floats, host or device. */
+som_status som_umatrix(som_ctx *h, float *U);
+
+/* Use the caller's CUDA stream (cudaStream_t as void*; NULL = the
+ * handle's own stream).  The caller keeps ownership of the stream. */
+som_status som_set_stream(som_ctx *h, void *cuda_stream);
+
+/* Device-side duration (CUDA events) of the main kernel(s) of the last
+ * call and how many steps or documents it processed. */
+som_status som_last_stats(som_ctx *h, double *ms, int64_t *units, int32_t *kernel_launches);
+
+/* Message for the last failure on this thread ("" if none). */
+const char *som_last_error(void);
+
+/* Build/version string, e.g. "libsom 0.1 sm_100a". */
+const char *som_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SOM_H */

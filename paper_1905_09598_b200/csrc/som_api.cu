@@ -1,0 +1,571 @@
+// som_api.cu — host runtime of libsom: validation, residency, staging of
+// host buffers, the decay table, launch sizing, timing.  Implements
+// include/som.h.  Product code: no oracle, no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/som.h"
+#include "som_device.cuh"
+#include "som_internal.h"
+
+using namespace som;
+
+namespace {
+
+thread_local std::string g_err;
+
+som_status fail(som_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(bytes, (size_t)256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct som_ctx {
+    int rows = 0, cols = 0, dim = 0, topo = 0, device = 0;
+    int N = 0;
+    float* W = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int sm_count = 0;
+    int max_smem_optin = 0;
+    bool poisoned = false;
+    int map_precision = SOM_MAP_AUTO;
+    int train_mode = SOM_TRAIN_AUTO;
+    // scratch
+    DevBuf xin;      // staged X / CSR
+    DevBuf xin2, xin3;
+    DevBuf keys;     // mapping top-2 keys
+    DevBuf outs;     // staged mapping outputs
+    DevBuf red;      // reduction partials
+    DevBuf ftab;     // decay table
+    DevBuf log;      // staged BMU log
+    DevBuf xchg;     // per-CTA exchange slots + abort flag
+    DevBuf dense;    // densified CSR chunk
+    // decay-table cache
+    int64_t f_T = -1, f_t0 = -1, f_t1 = -1;
+    int f_kind = -1;
+    double f_k = 0;
+    // timing
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0;
+    int64_t last_units = 0;
+    int last_launches = 0;
+};
+
+namespace {
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            h->poisoned = true;                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? SOM_ENOMEM : SOM_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+        }                                                                                     \
+    } while (0)
+
+#define CHECK_HANDLE(h)                                                                       \
+    do {                                                                                      \
+        if (!(h)) return fail(SOM_EINVAL, "null handle");                                    \
+        if ((h)->poisoned) return fail(SOM_ESTATE, "handle poisoned by an earlier CUDA failure"); \
+        cudaError_t e_ = cudaSetDevice((h)->device);                                          \
+        if (e_ != cudaSuccess) {                                                              \
+            (h)->poisoned = true;                                                             \
+            return fail(SOM_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e_));            \
+        }                                                                                     \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Make `src` (count bytes) available on the device: device pointers pass
+// through; host pointers are copied into `buf`.
+som_status stage_in(som_ctx* h, DevBuf& buf, const void* src, size_t bytes, const void** dev) {
+    if (is_device_ptr(src)) {
+        *dev = src;
+        return SOM_OK;
+    }
+    CK(buf.ensure(bytes));
+    CK(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    *dev = buf.p;
+    return SOM_OK;
+}
+
+// Decay factor table f_t, t in [t0, t1), of T steps (R1).  Computed on the
+// host in fp64 with the same expression order as the definition so the
+// device sees exactly the factors the definition gives; cached per
+// (T, kind, k, range).
+void fill_decay(double* out, int64_t t0, int64_t t1, int64_t T, int kind, double k) {
+    const double Td = (double)T;
+    const double e_k = std::exp(-k);
+    for (int64_t t = t0; t < t1; ++t) {
+        const double tau = (double)t / Td;
+        double f;
+        if (kind == SOM_DECAY_GAUSSIAN) f = std::exp(-k * tau * tau);
+        else if (kind == SOM_DECAY_LINEAR) f = 1.0 - (1.0 - e_k) * tau;
+        else f = std::exp(-k * tau);
+        out[t - t0] = f;
+    }
+}
+
+som_status ensure_decay_table(som_ctx* h, int64_t T, int kind, double k, int64_t t0, int64_t t1) {
+    if (h->f_T == T && h->f_kind == kind && h->f_k == k && h->f_t0 == t0 && h->f_t1 == t1) return SOM_OK;
+    const int64_t cnt = t1 - t0;
+    std::vector<double> host((size_t)cnt);
+    unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (cnt < 65536) nth = 1;
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nth; ++w) {
+        int64_t a = t0 + cnt * w / nth, b = t0 + cnt * (w + 1) / nth;
+        th.emplace_back(fill_decay, host.data() + (a - t0), a, b, T, kind, k);
+    }
+    for (auto& x : th) x.join();
+    CK(h->ftab.ensure(sizeof(double) * (size_t)std::max<int64_t>(cnt, 1)));
+    CK(cudaMemcpyAsync(h->ftab.p, host.data(), sizeof(double) * (size_t)cnt, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->f_T = T; h->f_kind = kind; h->f_k = k; h->f_t0 = t0; h->f_t1 = t1;
+    return SOM_OK;
+}
+
+uint64_t mulhi_host(uint64_t a, uint64_t b) { return (uint64_t)(((unsigned __int128)a * b) >> 64); }
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* som_last_error(void) { return g_err.c_str(); }
+
+const char* som_version(void) { return "libsom 0.1 sm_100a (persistent online SOM, exact map)"; }
+
+som_status som_schedule_default(som_schedule* s) {
+    if (!s) return fail(SOM_EINVAL, "null schedule");
+    s->kind = SOM_DECAY_GAUSSIAN;
+    s->k = std::log(100.0);
+    s->sigma_min = 1.0;
+    s->cutoff = 1e-4;
+    return SOM_OK;
+}
+
+som_status som_create(int32_t rows, int32_t cols, int32_t dim, int32_t topology, int32_t device, som_ctx** out) {
+    g_err.clear();
+    if (!out) return fail(SOM_EINVAL, "null out");
+    *out = nullptr;
+    if (rows < 1 || cols < 1 || dim < 1) return fail(SOM_EINVAL, "rows, cols, dim must be >= 1");
+    if ((int64_t)rows * cols > kMaxUnits) return fail(SOM_EINVAL, "rows*cols must be < 2^24");
+    if (topology != SOM_RECT && topology != SOM_HEX) return fail(SOM_EINVAL, "topology must be SOM_RECT or SOM_HEX");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(SOM_ECUDA, "no CUDA device (%s)", cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= ndev) return fail(SOM_EINVAL, "device %d out of range", device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(SOM_ECUDA, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SOM_ECUDA, "libsom is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+    som_ctx* h = new som_ctx();
+    h->rows = rows; h->cols = cols; h->dim = dim; h->topo = topology; h->device = device;
+    h->N = rows * cols;
+    h->sm_count = prop.multiProcessorCount;
+    h->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    auto bad = [&](cudaError_t err, const char* what) {
+        som_status st = fail(err == cudaErrorMemoryAllocation ? SOM_ENOMEM : SOM_ECUDA, "%s: %s", what,
+                             cudaGetErrorString(err));
+        som_destroy(h);
+        return st;
+    };
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return bad(e, "cudaSetDevice");
+    if ((e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking)) != cudaSuccess) return bad(e, "stream");
+    h->stream = h->own_stream;
+    if ((e = cudaMalloc(&h->W, sizeof(float) * (size_t)h->N * dim)) != cudaSuccess) return bad(e, "cudaMalloc W");
+    if ((e = cudaMemsetAsync(h->W, 0, sizeof(float) * (size_t)h->N * dim, h->stream)) != cudaSuccess) return bad(e, "memset");
+    if ((e = cudaEventCreate(&h->ev0)) != cudaSuccess) return bad(e, "event");
+    if ((e = cudaEventCreate(&h->ev1)) != cudaSuccess) return bad(e, "event");
+    if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return bad(e, "sync");
+    *out = h;
+    return SOM_OK;
+}
+
+void som_destroy(som_ctx* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense})
+        b->release();
+    if (h->W) cudaFree(h->W);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+}
+
+som_status som_set_stream(som_ctx* h, void* cuda_stream) {
+    CHECK_HANDLE(h);
+    CK(cudaStreamSynchronize(h->stream));
+    h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
+    return SOM_OK;
+}
+
+som_status som_set_weights(som_ctx* h, const float* w) {
+    CHECK_HANDLE(h);
+    if (!w) return fail(SOM_EINVAL, "null weights");
+    CK(cudaMemcpyAsync(h->W, w, sizeof(float) * (size_t)h->N * h->dim, cudaMemcpyDefault, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return SOM_OK;
+}
+
+som_status som_get_weights(som_ctx* h, float* w) {
+    CHECK_HANDLE(h);
+    if (!w) return fail(SOM_EINVAL, "null weights");
+    CK(cudaMemcpyAsync(w, h->W, sizeof(float) * (size_t)h->N * h->dim, cudaMemcpyDefault, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return SOM_OK;
+}
+
+som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed) {
+    CHECK_HANDLE(h);
+    if (!X) return fail(SOM_EINVAL, "null X");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0");
+    const int N = h->N;
+    std::vector<int64_t> idx((size_t)N);
+    if (N <= n) {
+        // Floyd's sampling without replacement, draws from SplitMix64(seed)
+        std::unordered_set<int64_t> taken;
+        taken.reserve((size_t)N * 2);
+        int64_t draw = 0, o = 0;
+        for (int64_t j = n - N; j < n; ++j) {
+            int64_t r = (int64_t)mulhi_host(splitmix64_at(seed, draw++), (uint64_t)(j + 1));
+            int64_t pick = taken.count(r) ? j : r;
+            taken.insert(pick);
+            idx[(size_t)o++] = pick;
+        }
+    } else {
+        for (int u = 0; u < N; ++u) idx[(size_t)u] = (int64_t)mulhi_host(splitmix64_at(seed, u), (uint64_t)n);
+    }
+    const size_t rowb = sizeof(float) * (size_t)h->dim;
+    if (is_device_ptr(X)) {
+        CK(h->keys.ensure(sizeof(int64_t) * (size_t)N));
+        CK(cudaMemcpyAsync(h->keys.p, idx.data(), sizeof(int64_t) * (size_t)N, cudaMemcpyHostToDevice, h->stream));
+        CK(launch_gather_rows(X, (const int64_t*)h->keys.p, N, h->dim, h->W, h->stream));
+    } else {
+        std::vector<float> rowsbuf((size_t)N * h->dim);
+        for (int u = 0; u < N; ++u) std::memcpy(rowsbuf.data() + (size_t)u * h->dim, X + idx[(size_t)u] * h->dim, rowb);
+        CK(cudaMemcpyAsync(h->W, rowsbuf.data(), rowb * (size_t)N, cudaMemcpyHostToDevice, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return SOM_OK;
+}
+
+som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epochs, double alpha0, double sigma0,
+                            const som_schedule* s, uint64_t seed, int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
+    CHECK_HANDLE(h);
+    som_schedule sd;
+    som_schedule_default(&sd);
+    if (s) sd = *s;
+    if (!X) return fail(SOM_EINVAL, "null X");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: no data to train on");
+    if (epochs < 0) return fail(SOM_EINVAL, "epochs must be >= 0");
+    if (!(alpha0 >= 0.0 && alpha0 <= 1.0)) return fail(SOM_EINVAL, "alpha0 must be in [0, 1]");
+    if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
+    if (sd.kind < 0 || sd.kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
+    if (!(sd.k > 0.0) || !std::isfinite(sd.k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
+    if (!(sd.sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
+    if (!(sd.cutoff >= 0.0 && sd.cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
+    const int64_t T = (int64_t)epochs * n;
+    if (t_end == -1) t_end = T;
+    if (t_begin < 0 || t_end < t_begin || t_end > T) return fail(SOM_EINVAL, "bad t-range [%lld, %lld) for T = %lld",
+                                                                 (long long)t_begin, (long long)t_end, (long long)T);
+    h->last_ms = 0; h->last_units = 0; h->last_launches = 0;
+    if (t_end == t_begin) return SOM_OK;   // epochs = 0 or empty range: weights unchanged
+
+    const void* Xd = nullptr;
+    som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
+    if (st) return st;
+    if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
+
+    // launch geometry: one persistent CTA per SM (at most one per unit)
+    TrainArgs a{};
+    a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
+    a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->N;
+    a.G = std::min(h->N, h->sm_count);
+    a.S = (h->N + a.G - 1) / a.G;
+    a.t0 = t_begin; a.t1 = t_end; a.seed = seed;
+    a.f_tab = (const double*)h->ftab.p;
+    a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
+    a.cutoff_on = sd.cutoff > 0.0;
+    a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
+    a.x_vec4 = (h->dim % 4 == 0) && ((uintptr_t)Xd % 16 == 0);
+    size_t smem = train_smem_bytes(a.S, a.dimp, 1);
+    a.w_smem = smem <= (size_t)h->max_smem_optin;
+    if (h->train_mode == SOM_TRAIN_W_SHARED && !a.w_smem)
+        return fail(SOM_EUNSUPPORTED, "W slice (%zu B/CTA) does not fit shared memory", smem);
+    if (h->train_mode == SOM_TRAIN_W_GLOBAL) a.w_smem = 0;
+    if (!a.w_smem) smem = train_smem_bytes(a.S, a.dimp, 0);
+    if (smem > (size_t)h->max_smem_optin)
+        return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
+
+    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.G + 64));
+    a.xchg = (unsigned long long*)h->xchg.p;
+    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.G);
+    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.G + 64, h->stream));
+
+    const int64_t steps = t_end - t_begin;
+    bool log_dev = bmu_log && is_device_ptr(bmu_log);
+    if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps));
+    a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
+
+    CK(cudaEventRecord(h->ev0, h->stream));
+    CK(launch_train(a, smem, h->stream));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if (bmu_log && !log_dev)
+        CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    unsigned abort_flag = 0;
+    CK(cudaMemcpy(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    if (abort_flag) {
+        h->poisoned = true;
+        return fail(SOM_ECUDA, "training exchange timed out (a CTA stopped publishing its BMU candidate)");
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = steps; h->last_launches = 1;
+    return SOM_OK;
+}
+
+som_status som_set_train_mode(som_ctx* h, int32_t mode) {
+    CHECK_HANDLE(h);
+    if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_W_GLOBAL) return fail(SOM_EINVAL, "unknown train mode");
+    h->train_mode = mode;
+    return SOM_OK;
+}
+
+som_status som_set_map_precision(som_ctx* h, int32_t precision) {
+    CHECK_HANDLE(h);
+    if (precision < SOM_MAP_AUTO || precision > SOM_MAP_3XTF32) return fail(SOM_EINVAL, "unknown map precision");
+    if (precision == SOM_MAP_3XTF32) return fail(SOM_EUNSUPPORTED, "3xTF32 mapping is not built yet");
+    h->map_precision = precision;
+    return SOM_OK;
+}
+
+namespace {
+
+// Map n rows of the device matrix Xd into device outputs (all device).
+som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches) {
+    const int tiles_m = map_exact_tiles_m(n);
+    const int tiles_n = map_exact_tiles_n(h->N);
+    int nsplit = std::max(1, std::min(tiles_n, (2 * h->sm_count + tiles_m - 1) / tiles_m));
+    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)nsplit * (size_t)n));
+    MapArgs a{h->W, h->N, Xd, n, h->dim, nsplit, (unsigned long long*)h->keys.p};
+    CK(launch_map_exact(a, h->stream));
+    CK(launch_map_merge(a.keys, nsplit, n, b1, b2, d2, h->stream));
+    *launches += 2;
+    return SOM_OK;
+}
+
+struct OutStage {
+    int32_t* b1 = nullptr; int32_t* b2 = nullptr; float* d2 = nullptr;
+    bool host1 = false, host2 = false, host3 = false;
+};
+
+som_status stage_outputs(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2, bool need_all, OutStage& o) {
+    o.host1 = bmu1 && !is_device_ptr(bmu1);
+    o.host2 = bmu2 && !is_device_ptr(bmu2);
+    o.host3 = d2 && !is_device_ptr(d2);
+    const size_t per = sizeof(int32_t) * 2 + sizeof(float);
+    CK(h->outs.ensure(per * (size_t)std::max<int64_t>(n, 1)));
+    char* base = (char*)h->outs.p;
+    o.b1 = (bmu1 && !o.host1) ? bmu1 : (int32_t*)base;
+    o.b2 = (bmu2 && !o.host2) ? bmu2 : ((bmu2 || need_all) ? (int32_t*)(base + sizeof(int32_t) * (size_t)n) : nullptr);
+    o.d2 = (d2 && !o.host3) ? d2 : ((d2 || need_all) ? (float*)(base + sizeof(int32_t) * 2 * (size_t)n) : nullptr);
+    return SOM_OK;
+}
+
+som_status copy_back(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2, const OutStage& o) {
+    if (o.host1) CK(cudaMemcpyAsync(bmu1, o.b1, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+    if (o.host2) CK(cudaMemcpyAsync(bmu2, o.b2, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+    if (o.host3) CK(cudaMemcpyAsync(d2, o.d2, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+    return SOM_OK;
+}
+
+}  // namespace
+
+som_status som_map(som_ctx* h, const float* X, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(SOM_EINVAL, "n < 0");
+    if (n == 0) return SOM_OK;   // S:240 empty matrix -> empty result
+    if (!X || !bmu1) return fail(SOM_EINVAL, "null X or bmu1");
+    const void* Xd = nullptr;
+    som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
+    if (st) return st;
+    OutStage o;
+    if ((st = stage_outputs(h, n, bmu1, bmu2, d2, false, o))) return st;
+    int launches = 0;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if ((st = map_dense_dev(h, (const float*)Xd, n, o.b1, o.b2, o.d2, &launches))) return st;
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if ((st = copy_back(h, n, bmu1, bmu2, d2, o))) return st;
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = n; h->last_launches = launches;
+    return SOM_OK;
+}
+
+som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                       int32_t* bmu1, int32_t* bmu2, float* d2) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(SOM_EINVAL, "n < 0");
+    if (n == 0) return SOM_OK;
+    if (!rowptr || !col || !val || !bmu1) return fail(SOM_EINVAL, "null CSR array or bmu1");
+    // nnz from rowptr[n] (host or device)
+    int64_t nnz = 0;
+    const bool rp_dev = is_device_ptr(rowptr);
+    if (rp_dev) CK(cudaMemcpy(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    else nnz = rowptr[n];
+    if (nnz < 0) return fail(SOM_EINVAL, "rowptr[n] < 0");
+    const void *rpd, *cd, *vd;
+    som_status st = stage_in(h, h->xin, rowptr, sizeof(int64_t) * (size_t)(n + 1), &rpd);
+    if (st) return st;
+    if ((st = stage_in(h, h->xin2, col, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1), &cd))) return st;
+    if ((st = stage_in(h, h->xin3, val, sizeof(float) * (size_t)std::max<int64_t>(nnz, 1), &vd))) return st;
+    OutStage o;
+    if ((st = stage_outputs(h, n, bmu1, bmu2, d2, false, o))) return st;
+    // densify in chunks of <= 1 GiB and map each chunk
+    const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));
+    CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim));
+    int launches = 0;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t m = std::min(chunk, n - r0);
+        CK(launch_densify((const int64_t*)rpd, (const int32_t*)cd, (const float*)vd, r0, m, h->dim, (float*)h->dense.p,
+                          h->stream));
+        ++launches;
+        if ((st = map_dense_dev(h, (const float*)h->dense.p, m, o.b1 + r0, o.b2 ? o.b2 + r0 : nullptr,
+                                o.d2 ? o.d2 + r0 : nullptr, &launches)))
+            return st;
+    }
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if ((st = copy_back(h, n, bmu1, bmu2, d2, o))) return st;
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = n; h->last_launches = launches;
+    return SOM_OK;
+}
+
+som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double* te) {
+    CHECK_HANDLE(h);
+    if (!X) return fail(SOM_EINVAL, "null X");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    const void* Xd = nullptr;
+    som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
+    if (st) return st;
+    OutStage o;
+    if ((st = stage_outputs(h, n, nullptr, nullptr, nullptr, true, o))) return st;
+    int launches = 0;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if ((st = map_dense_dev(h, (const float*)Xd, n, o.b1, o.b2, o.d2, &launches))) return st;
+    const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
+    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2)));
+    double* partial = (double*)h->red.p;
+    unsigned long long* pcnt = (unsigned long long*)(partial + nb);
+    double* osum = (double*)(pcnt + nb);
+    unsigned long long* obad = (unsigned long long*)(osum + 1);
+    CK(launch_errors(o.b1, o.b2, o.d2, n, h->rows, h->cols, h->topo, partial, pcnt, nb, osum, obad, h->stream));
+    launches += 2;
+    CK(cudaEventRecord(h->ev1, h->stream));
+    double sum = 0;
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&sum, osum, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(&bad, obad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (qe) *qe = sum / (double)n;
+    if (te) *te = (double)bad / (double)n;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = n; h->last_launches = launches;
+    return SOM_OK;
+}
+
+som_status som_qerror(som_ctx* h, const float* X, int64_t n, double* qe) {
+    if (!qe) return fail(SOM_EINVAL, "null qe");
+    return som_errors(h, X, n, qe, nullptr);
+}
+
+som_status som_topographic_error(som_ctx* h, const float* X, int64_t n, double* te) {
+    if (!te) return fail(SOM_EINVAL, "null te");
+    return som_errors(h, X, n, nullptr, te);
+}
+
+som_status som_umatrix(som_ctx* h, float* U) {
+    CHECK_HANDLE(h);
+    if (!U) return fail(SOM_EINVAL, "null U");
+    const bool dev = is_device_ptr(U);
+    float* Ud = U;
+    if (!dev) {
+        CK(h->outs.ensure(sizeof(float) * (size_t)h->N));
+        Ud = (float*)h->outs.p;
+    }
+    CK(cudaEventRecord(h->ev0, h->stream));
+    CK(launch_umatrix(h->W, h->rows, h->cols, h->topo, h->dim, Ud, h->stream));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if (!dev) CK(cudaMemcpyAsync(U, Ud, sizeof(float) * (size_t)h->N, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = h->N; h->last_launches = 1;
+    return SOM_OK;
+}
+
+som_status som_last_stats(som_ctx* h, double* ms, int64_t* units, int32_t* kernel_launches) {
+    if (!h) return fail(SOM_EINVAL, "null handle");
+    if (ms) *ms = h->last_ms;
+    if (units) *units = h->last_units;
+    if (kernel_launches) *kernel_launches = h->last_launches;
+    return SOM_OK;
+}
+
+}  // extern "C"

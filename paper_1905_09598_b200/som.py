@@ -1,0 +1,279 @@
+"""Thin Python binding of libsom (include/som.h): argument marshalling only.
+
+Every function has the name of the C entry point it calls and the same
+argument order.  Arrays may be numpy arrays (host memory) or torch tensors
+(host or CUDA); the library detects where each pointer lives.  All compute
+runs in libsom's sm_100a kernels — there is no Python or CPU fallback: if
+libsom.so is missing or no B200 is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsom.so")
+
+SOM_OK, SOM_EINVAL, SOM_EDIM, SOM_EEMPTY, SOM_ENOMEM, SOM_ECUDA, SOM_ENCCL, SOM_ESTATE, SOM_EUNSUPPORTED = range(9)
+SOM_RECT, SOM_HEX = 0, 1
+SOM_DECAY_GAUSSIAN, SOM_DECAY_LINEAR, SOM_DECAY_EXP = 0, 1, 2
+SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32 = 0, 1, 2
+SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL = 0, 1, 2
+
+_STATUS = {0: "SOM_OK", 1: "SOM_EINVAL", 2: "SOM_EDIM", 3: "SOM_EEMPTY", 4: "SOM_ENOMEM", 5: "SOM_ECUDA",
+           6: "SOM_ENCCL", 7: "SOM_ESTATE", 8: "SOM_EUNSUPPORTED"}
+
+
+class SomError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class som_schedule(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("k", ctypes.c_double), ("sigma_min", ctypes.c_double),
+                ("cutoff", ctypes.c_double)]
+
+
+_lib = None
+
+# every symbol include/som.h declares (tests check the library exports them)
+EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
+           "som_init_random", "som_train_online", "som_set_train_mode", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
+           "som_last_stats", "som_last_error", "som_version"]
+
+
+def lib():
+    """Load libsom.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    sig = {
+        "som_schedule_default": [P],
+        "som_create": [i32, i32, i32, i32, i32, P],
+        "som_set_weights": [P, P],
+        "som_get_weights": [P, P],
+        "som_init_random": [P, P, i64, u64],
+        "som_train_online": [P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
+        "som_map": [P, P, i64, P, P, P],
+        "som_map_csr": [P, P, P, P, i64, P, P, P],
+        "som_set_map_precision": [P, i32],
+        "som_set_train_mode": [P, i32],
+        "som_qerror": [P, P, i64, P],
+        "som_topographic_error": [P, P, i64, P],
+        "som_errors": [P, P, i64, P, P],
+        "som_umatrix": [P, P],
+        "som_set_stream": [P, P],
+        "som_last_stats": [P, P, P, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.som_destroy.argtypes = [P]
+    L.som_destroy.restype = None
+    L.som_last_error.argtypes = []
+    L.som_last_error.restype = ctypes.c_char_p
+    L.som_version.argtypes = []
+    L.som_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != SOM_OK:
+        raise SomError(st, lib().som_last_error().decode())
+
+
+def _ptr(a, dtype=None, writable=False):
+    """Raw pointer of a contiguous numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        if dtype is not None and a.dtype != np.dtype(dtype):
+            raise TypeError(f"expected {np.dtype(dtype)}, got {a.dtype}")
+        if writable and not a.flags.writeable:
+            raise ValueError("output array is read-only")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):   # torch.Tensor
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if dtype is not None:
+            want = {np.float32: "torch.float32", np.int32: "torch.int32", np.int64: "torch.int64"}[dtype]
+            if str(a.dtype) != want:
+                raise TypeError(f"expected {want}, got {a.dtype}")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+# ------------------------------------------------------------------ ABI calls
+def som_schedule_default() -> som_schedule:
+    s = som_schedule()
+    _check(lib().som_schedule_default(ctypes.byref(s)))
+    return s
+
+
+def som_create(rows: int, cols: int, dim: int, topology: int, device: int = 0) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(lib().som_create(rows, cols, dim, topology, device, ctypes.byref(h)))
+    return h
+
+
+def som_destroy(h) -> None:
+    lib().som_destroy(h)
+
+
+def som_set_weights(h, w) -> None:
+    _check(lib().som_set_weights(h, _ptr(w, np.float32)))
+
+
+def som_get_weights(h, w) -> None:
+    _check(lib().som_get_weights(h, _ptr(w, np.float32, writable=True)))
+
+
+def som_init_random(h, X, n: int, seed: int) -> None:
+    _check(lib().som_init_random(h, _ptr(X, np.float32), n, seed & (2**64 - 1)))
+
+
+def som_train_online(h, X, n: int, epochs: int, alpha0: float, sigma0: float, sched: som_schedule | None,
+                     seed: int, t_begin: int = 0, t_end: int = -1, bmu_log=None) -> None:
+    sp = ctypes.byref(sched) if sched is not None else None
+    _check(lib().som_train_online(h, _ptr(X, np.float32), n, epochs, alpha0, sigma0, sp, seed & (2**64 - 1),
+                                  t_begin, t_end, _ptr(bmu_log, np.int32, writable=True)))
+
+
+def som_map(h, X, n: int, bmu1, bmu2=None, d2=None) -> None:
+    _check(lib().som_map(h, _ptr(X, np.float32), n, _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True),
+                         _ptr(d2, np.float32, True)))
+
+
+def som_map_csr(h, rowptr, col, val, n: int, bmu1, bmu2=None, d2=None) -> None:
+    _check(lib().som_map_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                             _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True), _ptr(d2, np.float32, True)))
+
+
+def som_set_train_mode(h, mode: int) -> None:
+    _check(lib().som_set_train_mode(h, mode))
+
+
+def som_set_map_precision(h, precision: int) -> None:
+    _check(lib().som_set_map_precision(h, precision))
+
+
+def som_qerror(h, X, n: int) -> float:
+    q = ctypes.c_double()
+    _check(lib().som_qerror(h, _ptr(X, np.float32), n, ctypes.byref(q)))
+    return q.value
+
+
+def som_topographic_error(h, X, n: int) -> float:
+    t = ctypes.c_double()
+    _check(lib().som_topographic_error(h, _ptr(X, np.float32), n, ctypes.byref(t)))
+    return t.value
+
+
+def som_errors(h, X, n: int) -> tuple[float, float]:
+    q, t = ctypes.c_double(), ctypes.c_double()
+    _check(lib().som_errors(h, _ptr(X, np.float32), n, ctypes.byref(q), ctypes.byref(t)))
+    return q.value, t.value
+
+
+def som_umatrix(h, U) -> None:
+    _check(lib().som_umatrix(h, _ptr(U, np.float32, True)))
+
+
+def som_set_stream(h, stream) -> None:
+    """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
+    raw = None if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    _check(lib().som_set_stream(h, raw))
+
+
+def som_last_stats(h) -> tuple[float, int, int]:
+    ms, units, launches = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int32()
+    _check(lib().som_last_stats(h, ctypes.byref(ms), ctypes.byref(units), ctypes.byref(launches)))
+    return ms.value, units.value, launches.value
+
+
+def som_last_error() -> str:
+    return lib().som_last_error().decode()
+
+
+def som_version() -> str:
+    return lib().som_version().decode()
+
+
+# ----------------------------------------------------- convenience wrapper
+class SOM:
+    """Owning handle: ``SOM(rows, cols, dim, topology)``; methods call the ABI."""
+
+    def __init__(self, rows: int, cols: int, dim: int, topology: int = SOM_HEX, device: int = 0):
+        self.rows, self.cols, self.dim, self.topology = rows, cols, dim, topology
+        self.N = rows * cols
+        self.h = som_create(rows, cols, dim, topology, device)
+
+    def close(self):
+        if self.h:
+            som_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_weights(self, w):
+        som_set_weights(self.h, w)
+
+    def get_weights(self, out=None):
+        if out is None:
+            out = np.empty((self.N, self.dim), np.float32)
+        som_get_weights(self.h, out)
+        return out
+
+    def init_random(self, X, seed: int):
+        som_init_random(self.h, X, X.shape[0], seed)
+
+    def train_online(self, X, epochs: int, alpha0: float = 0.1, sigma0: float | None = None, seed: int = 1,
+                     kind: int = SOM_DECAY_GAUSSIAN, k: float = math.log(100.0), sigma_min: float = 1.0,
+                     cutoff: float = 1e-4, t_begin: int = 0, t_end: int = -1, bmu_log=None):
+        if sigma0 is None:
+            sigma0 = max(self.rows, self.cols) / 2.0
+        s = som_schedule(kind, k, sigma_min, cutoff)
+        som_train_online(self.h, X, X.shape[0], epochs, alpha0, sigma0, s, seed, t_begin, t_end, bmu_log)
+        return bmu_log
+
+    def map(self, X, want_bmu2: bool = True, want_d2: bool = True):
+        n = X.shape[0]
+        b1 = np.empty(n, np.int32)
+        b2 = np.empty(n, np.int32) if want_bmu2 else None
+        d2 = np.empty(n, np.float32) if want_d2 else None
+        som_map(self.h, X, n, b1, b2, d2)
+        return b1, b2, d2
+
+    def errors(self, X):
+        return som_errors(self.h, X, X.shape[0])
+
+    def umatrix(self):
+        U = np.empty(self.N, np.float32)
+        som_umatrix(self.h, U)
+        return U
+
+    def last_stats(self):
+        return som_last_stats(self.h)

@@ -1,0 +1,75 @@
+"""The C-ABI boundary: libsom.so builds, loads and exports every entry point
+include/som.h declares; without a GPU it fails loudly (no CPU fallback).
+No compute calls here (CPU box)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "som.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(som_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1905_09598_b200 import _build
+    _build.build()
+    from paper_1905_09598_b200 import som
+    return som.lib()
+
+
+def test_header_declares_the_north_star_calls():
+    decl = _declared()
+    for name in ["som_create", "som_train_online", "som_map", "som_qerror", "som_umatrix",
+                 "som_topographic_error", "som_map_csr", "som_last_error"]:
+        assert name in decl
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1905_09598_b200 import som
+    decl = _declared()
+    missing = [s for s in decl if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(som.EXPORTS) == decl           # the binding covers the same set
+
+
+def test_binding_has_same_names():
+    from paper_1905_09598_b200 import som
+    for s in _declared():
+        assert callable(getattr(som, s)), s
+
+
+def test_schedule_defaults_and_validation_without_gpu(lib):
+    from paper_1905_09598_b200 import som
+    s = som.som_schedule_default()
+    assert s.kind == 0 and abs(s.k - 4.605170185988091) < 1e-15 and s.sigma_min == 1.0 and s.cutoff == 1e-4
+    h = ctypes.c_void_p()
+    assert lib.som_create(0, 3, 4, 0, 0, ctypes.byref(h)) == som.SOM_EINVAL
+    assert lib.som_create(3, 3, 4, 7, 0, ctypes.byref(h)) == som.SOM_EINVAL
+    assert lib.som_train_online(None, None, 1, 1, 0.1, 1.0, None, 1, 0, -1, None) == som.SOM_EINVAL
+    assert "version" not in som.som_version() and "sm_100a" in som.som_version()
+
+
+def test_fails_loudly_without_device(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1905_09598_b200 import som
+    with pytest.raises(som.SomError) as e:
+        som.som_create(2, 2, 4, som.SOM_HEX)
+    assert e.value.status == som.SOM_ECUDA
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1905_09598_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "som_oracle" not in txt, f
