@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py — the CUDASOM hot path on B200, one JSON line on rank 0.
+
+A "step" is one pass of the whole hot path over
+one synthetic c2 workload (BASELINE.json configs[1]): 20x20 hex map,
+5,000 x 3,000 L2-normalised TF-IDF corpus, 100 epochs of online training
+(T = 500,000 samples) from a seeded row init, then batch mapping of all
+documents, QE + TE, and the U-matrix.  value = training samples/s over the
+whole step, summed over ranks (each rank runs its own independent problem:
+weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference ...   # the oracle (CPU) on a bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, bank_corpus  # noqa: E402
+
+METRIC = "SOM training samples/sec and batch BMU-mapping docs/sec at 1/2/4/8 B200"
+ALPHA0 = 0.1
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    p.add_argument("--epochs", type=int, default=None, help="override epochs (diagnostics only)")
+    p.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--seed", type=int, default=1)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(cfg_name, seed, epochs_override):
+    cfg = dict(CONFIGS[cfg_name])
+    if epochs_override is not None:
+        cfg["epochs"] = epochs_override
+    C = bank_corpus(cfg["n"], cfg["d"], seed=seed)
+    return cfg, C
+
+
+def fp64_peak_tflops():
+    """Measured DFMA peak (profiles/probe_*.json), else the nominal B200 figure."""
+    path = os.path.join(ROOT, "profiles", "probe_fp64.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["dfma_tflops"]), "measured (profiles/probe_fp64.json)"
+    return 37.0, "nominal B200 FP64 (vendor), no measurement yet"
+
+
+# ------------------------------------------------------------- oracle legs
+def oracle_train_rate(cfg, X, W0, seed, steps):
+    import oracle
+    T = cfg["epochs"] * cfg["n"]
+    t0 = time.perf_counter()
+    oracle.train_online(W0, cfg["rows"], cfg["cols"], cfg["topo"], X, cfg["epochs"], ALPHA0, cfg["sigma0"],
+                        seed, t_begin=0, t_end=min(steps, T))
+    dt = time.perf_counter() - t0
+    return min(steps, T) / dt, dt, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    cfg, C = workload(args.config, args.seed, args.epochs)
+    X = C.dense()
+    from synth import init_rows
+    W0 = init_rows(X, cfg["rows"] * cfg["cols"], args.seed + 1000)
+    steps_per = {"c1": 2000, "c2": 400, "c3": 10}[args.config]
+    for _ in range(args.warmup):
+        oracle_train_rate(cfg, X, W0, args.seed, max(1, steps_per // 4))
+    rates, secs = [], 0.0
+    for _ in range(args.steps):
+        r, dt, nt = oracle_train_rate(cfg, X, W0, args.seed, steps_per)
+        rates.append(r)
+        secs += dt
+    v = args.steps * steps_per / secs
+    sample = (f"first {steps_per} of {cfg['epochs'] * cfg['n']} training steps of {args.config} per step "
+              f"(fp64 oracle, OpenMP over units)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, **cfg},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": nt, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- B200 leg
+def run_b200(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_09598_b200 import som
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seed = args.seed + rank                     # independent problem per rank
+    cfg, C = workload(args.config, seed, args.epochs)
+    n, d, N = cfg["n"], cfg["d"], cfg["rows"] * cfg["cols"]
+    T = cfg["epochs"] * n
+    X_host = torch.from_numpy(C.dense()).pin_memory()
+    X = X_host.cuda()
+    stream = torch.cuda.current_stream()
+    m = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+    som.som_set_stream(m.h, stream)
+    b1 = torch.empty(n, dtype=torch.int32, device="cuda")
+    b2 = torch.empty(n, dtype=torch.int32, device="cuda")
+    d1 = torch.empty(n, dtype=torch.float32, device="cuda")
+    U = torch.empty(N, dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+    sched = som.som_schedule_default()
+
+    def one_step(Xs, b1s, b2s, d1s, Us):
+        """The whole hot path once; returns per-phase kernel ms and launches."""
+        ph, launches = {}, 0
+        som.som_init_random(m.h, Xs, n, seed + 1000)
+        ms, _, l = som.som_last_stats(m.h)
+        launches += 1 if Xs.is_cuda else 0
+        som.som_train_online(m.h, Xs, n, cfg["epochs"], ALPHA0, cfg["sigma0"], sched, seed, 0, -1, None)
+        ph["train_ms"], _, l = som.som_last_stats(m.h)
+        launches += l
+        som.som_map(m.h, Xs, n, b1s, b2s, d1s)
+        ph["map_ms"], _, l = som.som_last_stats(m.h)
+        launches += l
+        qe, te = som.som_errors(m.h, Xs, n)
+        ph["errors_ms"], _, l = som.som_last_stats(m.h)
+        launches += l
+        som.som_umatrix(m.h, Us)
+        ph["umatrix_ms"], _, l = som.som_last_stats(m.h)
+        launches += l
+        return ph, launches, qe, te
+
+    for _ in range(args.warmup):
+        one_step(X, b1, b2, d1, U)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device resident inputs
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phases, launches = [], 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        w0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()                      # L2 flush between timed steps (not timed)
+            ev[i][0].record(stream)
+            ph, l, qe, te = one_step(X, b1, b2, d1, U)
+            ev[i][1].record(stream)
+            phases.append(ph)
+            launches += l
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    total_ms = float(t_max.item())
+    value = world * args.steps * T / (total_ms / 1000.0)
+
+    # ---- e2e: same step through the C ABI with pinned HOST buffers
+    b1h = torch.empty(n, dtype=torch.int32).pin_memory()
+    b2h = torch.empty(n, dtype=torch.int32).pin_memory()
+    d1h = torch.empty(n, dtype=torch.float32).pin_memory()
+    Uh = torch.empty(N, dtype=torch.float32).pin_memory()
+    Wh = torch.empty(N, d, dtype=torch.float32).pin_memory()
+    e2e_ms = []
+    for i in range(max(1, min(args.steps, 3))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        one_step(X_host, b1h, b2h, d1h, Uh)
+        som.som_get_weights(m.h, Wh)
+        torch.cuda.synchronize()
+        e2e_ms.append(1000 * (time.perf_counter() - t0))
+    e2e_t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    xb = n * d * 4
+    h2d = 3 * xb                               # X staged by train, map and errors
+    d2h = n * 4 * 2 + n * 4 + N * 4 + N * d * 4 + 16
+
+    # ---- roofline of the dominant kernel (the persistent training kernel)
+    train_ms = statistics.mean(p["train_ms"] for p in phases)
+    flop_per_sample = 3.0 * N * d               # fp64 distance: sub + fma per element (R10)
+    achieved = flop_per_sample * T / (train_ms / 1000.0) / 1e12
+    peak, peak_src = fp64_peak_tflops()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+
+    cpu = None
+    if not args.no_baseline:
+        import oracle
+        from synth import init_rows
+        Xn = X_host.numpy()
+        W0 = init_rows(Xn, N, seed + 1000)
+        steps_s = {"c1": 2000, "c2": 2000, "c3": 20}[args.config]
+        r, dt, nt = oracle_train_rate(cfg, Xn, W0, seed, steps_s)
+        cpu = {"value": r, "unit": "samples/s", "cores": nt, "kind": "oracle",
+               "sample": f"first {steps_s} of {T} training steps of {args.config} ({dt:.1f} s, fp64 oracle, "
+                         f"OpenMP over units)"}
+
+    ph_mean = {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64-acc/f32",
+        "data": "synthetic (seeded bank-shaped TF-IDF, synth/corpus.py)",
+        "config": {"workload": args.config, "map": f"{cfg['rows']}x{cfg['cols']} {'hex' if cfg['topo'] else 'rect'}",
+                   "docs": n, "terms": d, "epochs": cfg["epochs"], "samples_per_step": T,
+                   "alpha0": ALPHA0, "sigma0": cfg["sigma0"], "cutoff": 1e-4, "parallelism": f"replicas{world}",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "secondary": {"map_docs_per_s": n / (ph_mean["map_ms"] / 1000.0),
+                      "train_samples_per_s_kernel": T / (train_ms / 1000.0),
+                      "us_per_training_step": 1000.0 * train_ms / T, "phase_ms": ph_mean,
+                      "qe": qe, "te": te, "wall_s": wall},
+        "e2e": {"value": world * T / (float(e2e_t.item()) / 1000.0), "unit": "samples/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "alu", "kernel": "som_train_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "work": "3*N*d fp64 flop per sample (difference + fused square-accumulate)"},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
