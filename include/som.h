@@ -119,10 +119,22 @@ som_status som_train_online(som_ctx *h, const float *X, int64_t n, int32_t epoch
 
 /* Where som_train_online keeps each CTA's prototypes between steps:
  * AUTO picks shared memory when a CTA's share of W fits (else global
- * memory, L2-resident when W fits the L2).  Forcing SHARED for a map that
- * does not fit returns SOM_EUNSUPPORTED from som_train_online. */
-typedef enum { SOM_TRAIN_AUTO = 0, SOM_TRAIN_W_SHARED = 1, SOM_TRAIN_W_GLOBAL = 2 } som_train_mode;
+ * memory, L2-resident when W fits the L2); REGISTERS keeps each CTA's share
+ * in registers (small maps, d % 4 == 0).  Forcing a placement that does not
+ * fit returns SOM_EUNSUPPORTED from som_train_online. */
+typedef enum {
+    SOM_TRAIN_AUTO = 0, SOM_TRAIN_W_SHARED = 1, SOM_TRAIN_W_GLOBAL = 2, SOM_TRAIN_W_REGISTERS = 3
+} som_train_mode;
 som_status som_set_train_mode(som_ctx *h, int32_t mode);
+
+/* Number of persistent CTAs som_train_online uses (0 = automatic: a model
+ * of the per-step all-gather latency vs the per-CTA distance work).  Values
+ * above min(N, #SMs) are clamped.  Results do not depend on it. */
+som_status som_set_train_grid(som_ctx *h, int32_t grid);
+
+/* Grid and kernel variant of the last som_train_online call:
+ * kernel 0 = W in global memory, 1 = W in shared memory, 2 = W in registers. */
+som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* Batch mapping ("assigned each document vector to the best matching
  * vector on the trained map"): for each row, bmu1 = argmin (D,u),

@@ -66,6 +66,8 @@ struct som_ctx {
     bool poisoned = false;
     int map_precision = SOM_MAP_AUTO;
     int train_mode = SOM_TRAIN_AUTO;
+    int train_grid = 0;       // 0 = auto
+    int last_grid = 0, last_kernel = -1;
     // scratch
     DevBuf xin;      // staged X / CSR
     DevBuf xin2, xin3;
@@ -326,24 +328,50 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     if (st) return st;
     if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
 
-    // launch geometry: one persistent CTA per SM (at most one per unit)
     TrainArgs a{};
     a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
     a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->N;
-    a.G = std::min(h->N, h->sm_count);
+    a.x_vec4 = (h->dim % 4 == 0) && ((uintptr_t)Xd % 16 == 0);
+    // launch geometry.  Register-resident kernel when a CTA's share of W fits
+    // the register file: G minimises (all-gather latency + fp64 distance
+    // time), both measured on B200 (profiles/probe_*_r01.json).  Otherwise
+    // one persistent CTA per SM with W in shared or global memory.
+    bool use_reg = false;
+    if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
+        auto xchg_us = [](int G) { return G <= 32 ? 0.58 : G <= 64 ? 0.67 : G <= 128 ? 1.05 : 1.64; };
+        double best = 1e30;
+        int bestG = 0;
+        const int gmax = std::min(h->N, h->sm_count);
+        int cands[] = {gmax, 16, 24, 32, 48, 64, 96, 128};
+        for (int G : cands) {
+            if (h->train_grid > 0) G = h->train_grid;
+            if (G < 1 || G > gmax) continue;
+            const int S = (h->N + G - 1) / G;
+            if (!train_reg_supported(S, h->dim)) continue;
+            const double est = xchg_us(G) + (double)h->N * h->dim / ((double)G * 1.2e5);
+            if (est < best) { best = est; bestG = G; }
+        }
+        if (bestG > 0) { use_reg = true; a.G = bestG; }
+    }
+    if (h->train_mode == SOM_TRAIN_W_REGISTERS && !use_reg)
+        return fail(SOM_EUNSUPPORTED, "map share per CTA does not fit registers (or d %% 4 != 0)");
+    if (!use_reg) {
+        a.G = std::min(h->N, h->sm_count);
+        if (h->train_grid > 0) a.G = std::min(a.G, h->train_grid);
+    }
     a.S = (h->N + a.G - 1) / a.G;
     a.t0 = t_begin; a.t1 = t_end; a.seed = seed;
     a.f_tab = (const double*)h->ftab.p;
     a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
     a.cutoff_on = sd.cutoff > 0.0;
     a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
-    a.x_vec4 = (h->dim % 4 == 0) && ((uintptr_t)Xd % 16 == 0);
     size_t smem = train_smem_bytes(a.S, a.dimp, 1);
     a.w_smem = smem <= (size_t)h->max_smem_optin;
     if (h->train_mode == SOM_TRAIN_W_SHARED && !a.w_smem)
         return fail(SOM_EUNSUPPORTED, "W slice (%zu B/CTA) does not fit shared memory", smem);
     if (h->train_mode == SOM_TRAIN_W_GLOBAL) a.w_smem = 0;
     if (!a.w_smem) smem = train_smem_bytes(a.S, a.dimp, 0);
+    if (use_reg) smem = sizeof(float) * 3 * (size_t)a.dimp;
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
 
@@ -358,8 +386,11 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
 
     CK(cudaEventRecord(h->ev0, h->stream));
-    CK(launch_train(a, smem, h->stream));
+    if (use_reg) CK(launch_train_reg(a, h->stream));
+    else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
+    h->last_grid = a.G;
+    h->last_kernel = use_reg ? 2 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -377,8 +408,22 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
 
 som_status som_set_train_mode(som_ctx* h, int32_t mode) {
     CHECK_HANDLE(h);
-    if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_W_GLOBAL) return fail(SOM_EINVAL, "unknown train mode");
+    if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_W_REGISTERS) return fail(SOM_EINVAL, "unknown train mode");
     h->train_mode = mode;
+    return SOM_OK;
+}
+
+som_status som_set_train_grid(som_ctx* h, int32_t grid) {
+    CHECK_HANDLE(h);
+    if (grid < 0) return fail(SOM_EINVAL, "grid must be >= 0 (0 = auto)");
+    h->train_grid = grid;
+    return SOM_OK;
+}
+
+som_status som_last_train_config(som_ctx* h, int32_t* grid, int32_t* kernel) {
+    if (!h) return fail(SOM_EINVAL, "null handle");
+    if (grid) *grid = h->last_grid;
+    if (kernel) *kernel = h->last_kernel;
     return SOM_OK;
 }
 

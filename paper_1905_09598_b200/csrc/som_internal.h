@@ -37,6 +37,10 @@ struct TrainArgs {
 
 size_t train_smem_bytes(int S, int dimp, int w_smem);
 cudaError_t launch_train(const TrainArgs& a, size_t smem, cudaStream_t st);
+// register-resident variant (train_reg.cu): needs d % 4 == 0 and a small
+// per-CTA share of W (S units x ceil(d/2048) float4 chunks per thread).
+bool train_reg_supported(int S, int dim);
+cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st);
 
 // Exact (fp64-accumulated) batch mapping: partial top-2 keys per doc per
 // neuron split, then merged.  keys: [nsplit][n][2] u64 scratch.

@@ -21,7 +21,7 @@ SOM_OK, SOM_EINVAL, SOM_EDIM, SOM_EEMPTY, SOM_ENOMEM, SOM_ECUDA, SOM_ENCCL, SOM_
 SOM_RECT, SOM_HEX = 0, 1
 SOM_DECAY_GAUSSIAN, SOM_DECAY_LINEAR, SOM_DECAY_EXP = 0, 1, 2
 SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32 = 0, 1, 2
-SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL = 0, 1, 2
+SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL, SOM_TRAIN_W_REGISTERS = 0, 1, 2, 3
 
 _STATUS = {0: "SOM_OK", 1: "SOM_EINVAL", 2: "SOM_EDIM", 3: "SOM_EEMPTY", 4: "SOM_ENOMEM", 5: "SOM_ECUDA",
            6: "SOM_ENCCL", 7: "SOM_ESTATE", 8: "SOM_EUNSUPPORTED"}
@@ -42,7 +42,7 @@ _lib = None
 
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
-           "som_init_random", "som_train_online", "som_set_train_mode", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_init_random", "som_train_online", "som_set_train_mode", "som_set_train_grid", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
            "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version"]
 
@@ -67,6 +67,8 @@ def lib():
         "som_map_csr": [P, P, P, P, i64, P, P, P],
         "som_set_map_precision": [P, i32],
         "som_set_train_mode": [P, i32],
+        "som_set_train_grid": [P, i32],
+        "som_last_train_config": [P, P, P],
         "som_qerror": [P, P, i64, P],
         "som_topographic_error": [P, P, i64, P],
         "som_errors": [P, P, i64, P, P],
@@ -164,6 +166,16 @@ def som_map_csr(h, rowptr, col, val, n: int, bmu1, bmu2=None, d2=None) -> None:
 
 def som_set_train_mode(h, mode: int) -> None:
     _check(lib().som_set_train_mode(h, mode))
+
+
+def som_set_train_grid(h, grid: int) -> None:
+    _check(lib().som_set_train_grid(h, grid))
+
+
+def som_last_train_config(h) -> tuple[int, int]:
+    g, k = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().som_last_train_config(h, ctypes.byref(g), ctypes.byref(k)))
+    return g.value, k.value
 
 
 def som_set_map_precision(h, precision: int) -> None:

@@ -207,3 +207,41 @@ def test_validation_errors(som):
         assert e.value.status == som.SOM_EEMPTY
         # the handle still works after argument errors
         m.train_online(X, epochs=1, alpha0=0.1, sigma0=1.0, seed=1)
+
+
+@pytest.mark.parametrize("grid", [1, 7, 32, 64, 148])
+def test_register_kernel_grid_invariance(som, grid):
+    """Results do not depend on the number of persistent CTAs."""
+    C = bank_corpus(400, 1200, seed=12)
+    X = C.dense()
+    W0 = init_rows(X, 80, 12)
+    with som.SOM(8, 10, 1200, 1) as m:
+        som.som_set_train_mode(m.h, som.SOM_TRAIN_W_REGISTERS if grid >= 10 else som.SOM_TRAIN_AUTO)
+        som.som_set_train_grid(m.h, grid)
+        m.set_weights(W0)
+        log = np.empty(1600, np.int32)
+        m.train_online(X, epochs=4, alpha0=0.1, sigma0=5.0, seed=12, bmu_log=log)
+        W = m.get_weights()
+        g, kern = som.som_last_train_config(m.h)
+    assert g == min(grid, 80)
+    Wo, logo = oracle.train_online(W0, 8, 10, 1, X, 4, 0.1, 5.0, 12)
+    _assert_train(W, log, Wo, logo)
+
+
+def test_c2_kernel_variants_agree(som):
+    """c2 shape, 3000 steps: register, shared and global placements give the same result."""
+    C = bank_corpus(5000, 3000, seed=2)
+    X = C.dense()
+    W0 = init_rows(X, 400, 1002)
+    out = {}
+    for mode in (som.SOM_TRAIN_W_REGISTERS, som.SOM_TRAIN_W_SHARED, som.SOM_TRAIN_W_GLOBAL):
+        with som.SOM(20, 20, 3000, 1) as m:
+            som.som_set_train_mode(m.h, mode)
+            m.set_weights(W0)
+            log = np.empty(3000, np.int32)
+            m.train_online(X, epochs=100, alpha0=0.1, sigma0=10.0, seed=2, t_end=3000, bmu_log=log)
+            out[mode] = (m.get_weights(), log, som.som_last_train_config(m.h))
+    W1, l1, c1 = out[som.SOM_TRAIN_W_REGISTERS]
+    assert c1[1] == 2
+    for mode in (som.SOM_TRAIN_W_SHARED, som.SOM_TRAIN_W_GLOBAL):
+        assert np.array_equal(out[mode][1], l1) and np.array_equal(out[mode][0], W1)
