@@ -136,6 +136,14 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * kernel 0 = W in global memory, 1 = W in shared memory, 2 = W in registers. */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
+/* Phase trace of the register-resident training kernel (profiling aid):
+ * device_buf (device memory, 148 * steps * 8 uint64, layout [CTA][step][8])
+ * receives %globaltimer (ns) at 8 phase boundaries of the first `steps`
+ * steps of every CTA (loop top, fused pass done, partials ready, key
+ * published, winner known, neighbourhood ready, x staged, step end).
+ * NULL disables. */
+som_status som_set_trace(som_ctx *h, void *device_buf, int32_t steps);
+
 /* Batch mapping ("assigned each document vector to the best matching
  * vector on the trained map"): for each row, bmu1 = argmin (D,u),
  * bmu2 = argmin over u != bmu1 (-1 if N = 1), d2 = D at bmu1 (squared

@@ -68,6 +68,8 @@ struct som_ctx {
     int train_mode = SOM_TRAIN_AUTO;
     int train_grid = 0;       // 0 = auto
     int last_grid = 0, last_kernel = -1;
+    unsigned long long* trace = nullptr;   // caller-owned device buffer (som_set_trace)
+    int trace_steps = 0;
     // scratch
     DevBuf xin;      // staged X / CSR
     DevBuf xin2, xin3;
@@ -338,17 +340,20 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     // one persistent CTA per SM with W in shared or global memory.
     bool use_reg = false;
     if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
-        auto xchg_us = [](int G) { return G <= 32 ? 0.58 : G <= 64 ? 0.67 : G <= 128 ? 1.05 : 1.64; };
+        // all-gather latency by grid size (profiles/probe_xchg_r01.json) and
+        // per-CTA F2F-bound distance time: (S + 1) * d conversions at 16/clk
+        auto xchg_us = [](int G) { return G <= 32 ? 0.70 : G <= 64 ? 0.72 : G <= 128 ? 0.90 : 1.65; };
         double best = 1e30;
         int bestG = 0;
         const int gmax = std::min(h->N, h->sm_count);
-        int cands[] = {gmax, 16, 24, 32, 48, 64, 96, 128};
+        std::vector<int> cands = {gmax, 16, 24, 32, 48, 64, 96, 128};
+        for (int S = 1; S <= 8; ++S) cands.push_back((h->N + S - 1) / S);   // balanced grids
         for (int G : cands) {
-            if (h->train_grid > 0) G = h->train_grid;
+            if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
             if (G < 1 || G > gmax) continue;
             const int S = (h->N + G - 1) / G;
             if (!train_reg_supported(S, h->dim)) continue;
-            const double est = xchg_us(G) + (double)h->N * h->dim / ((double)G * 1.2e5);
+            const double est = xchg_us(G) + (double)(S + 1) * h->dim / (16.0 * 1965.0);
             if (est < best) { best = est; bestG = G; }
         }
         if (bestG > 0) { use_reg = true; a.G = bestG; }
@@ -365,6 +370,8 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
     a.cutoff_on = sd.cutoff > 0.0;
     a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
+    a.trace = h->trace;
+    a.trace_steps = h->trace ? h->trace_steps : 0;
     size_t smem = train_smem_bytes(a.S, a.dimp, 1);
     a.w_smem = smem <= (size_t)h->max_smem_optin;
     if (h->train_mode == SOM_TRAIN_W_SHARED && !a.w_smem)
@@ -410,6 +417,15 @@ som_status som_set_train_mode(som_ctx* h, int32_t mode) {
     CHECK_HANDLE(h);
     if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_W_REGISTERS) return fail(SOM_EINVAL, "unknown train mode");
     h->train_mode = mode;
+    return SOM_OK;
+}
+
+som_status som_set_trace(som_ctx* h, void* device_buf, int32_t steps) {
+    CHECK_HANDLE(h);
+    if (device_buf && (steps < 1 || !is_device_ptr(device_buf)))
+        return fail(SOM_EINVAL, "trace buffer must be device memory with steps >= 1");
+    h->trace = (unsigned long long*)device_buf;
+    h->trace_steps = device_buf ? steps : 0;
     return SOM_OK;
 }
 

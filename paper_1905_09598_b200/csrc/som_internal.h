@@ -33,7 +33,17 @@ struct TrainArgs {
     int32_t* bmu_log;          // nullable, (t1 - t0) entries, device
     int w_smem;                // 1: the CTA's W rows live in shared memory
     int x_vec4;                // 1: X rows are 16-byte aligned (d % 4 == 0)
+    unsigned long long* trace; // nullable: [G][trace_steps][kTracePhases] globaltimer (ns) per CTA
+    int trace_steps;
 };
+
+constexpr int kTracePhases = 8;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 size_t train_smem_bytes(int S, int dimp, int w_smem);
 cudaError_t launch_train(const TrainArgs& a, size_t smem, cudaStream_t st);

@@ -42,7 +42,7 @@ _lib = None
 
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
-           "som_init_random", "som_train_online", "som_set_train_mode", "som_set_train_grid", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_init_random", "som_train_online", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
            "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version"]
 
@@ -68,6 +68,7 @@ def lib():
         "som_set_map_precision": [P, i32],
         "som_set_train_mode": [P, i32],
         "som_set_train_grid": [P, i32],
+        "som_set_trace": [P, P, i32],
         "som_last_train_config": [P, P, P],
         "som_qerror": [P, P, i64, P],
         "som_topographic_error": [P, P, i64, P],
@@ -166,6 +167,10 @@ def som_map_csr(h, rowptr, col, val, n: int, bmu1, bmu2=None, d2=None) -> None:
 
 def som_set_train_mode(h, mode: int) -> None:
     _check(lib().som_set_train_mode(h, mode))
+
+
+def som_set_trace(h, device_buf, steps: int) -> None:
+    _check(lib().som_set_trace(h, _ptr(device_buf), steps))
 
 
 def som_set_train_grid(h, grid: int) -> None:

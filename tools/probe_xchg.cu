@@ -51,6 +51,35 @@ __global__ void p_gather(unsigned long long* slots, int steps, int stride, unsig
     if (threadIdx.x == 0 && acc == 42) out[0] = acc;
 }
 
+// P0r: R replicas of the tagged slot array; CTA b writes its key into every
+// replica (lanes over replicas) and polls replica b % R.  R = G is a private
+// mailbox per CTA.  Replica r lives at slots + r * 2 * G * stride_r.
+__global__ void p_gather_rep(unsigned long long* slots, int steps, int R, unsigned long long* out) {
+    const int G = gridDim.x, b = blockIdx.x, lane = threadIdx.x & 31;
+    const size_t rep_stride = ((size_t)2 * G + 31) & ~(size_t)31;   // 256 B aligned replicas
+    unsigned long long acc = 0;
+    for (int t = 0; t < steps; ++t) {
+        if (threadIdx.x < 32) {
+            const unsigned long long tag = 0x80ull | (unsigned long long)(t & 0x7F);
+            const unsigned long long key = ((unsigned long long)((b * 7 + t) % 1000) << 8) | tag;
+            for (int r = lane; r < R; r += 32) st_relaxed_u64(slots + r * rep_stride + (size_t)(t & 1) * G + b, key);
+            const unsigned long long* s = slots + (size_t)(b % R) * rep_stride + (size_t)(t & 1) * G;
+            for (;;) {
+                unsigned long long m = ~0ull;
+                bool ok = true;
+                for (int j = lane; j < G; j += 32) {
+                    unsigned long long v = ld_relaxed_u64(s + j);
+                    ok &= (v & 0xFF) == tag;
+                    m = umin(m, v);
+                }
+                if (__all_sync(0xffffffffu, ok)) { acc += m; break; }
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && acc == 42) out[0] = acc;
+}
+
 // P1: atomicMin into slot[t%3] + release-add arrival counter; poll counter (acquire), read slot
 __global__ void p_atomic(unsigned long long* slot3, unsigned* cnt3, int steps, unsigned long long* out) {
     const int G = gridDim.x, b = blockIdx.x;
@@ -155,6 +184,23 @@ int main() {
                 CK(cudaLaunchCooperativeKernel((void*)p_gather, G, 512, a, 0, 0));
             });
             printf("  \"gather_stride%d_G%d\": %.3f,\n", stride, G, us);
+        }
+    }
+    {
+        unsigned long long* rep;
+        const size_t rep_bytes = (size_t)148 * 320 * 8;
+        CK(cudaMalloc(&rep, rep_bytes));
+        for (int G : {148, 128, 64, 32}) {
+            for (int R : {1, 2, 4, 8, 16, 32, 64, 148}) {
+                if (R > G) continue;
+                float us = timeit([&] {
+                    CK(cudaMemset(rep, 0, rep_bytes));
+                    int st = steps, r = R;
+                    void* a[] = {&rep, &st, &r, &out};
+                    CK(cudaLaunchCooperativeKernel((void*)p_gather_rep, G, 512, a, 0, 0));
+                });
+                printf("  \"rep%d_G%d\": %.3f,\n", R, G, us);
+            }
         }
     }
     for (int G : {148, 74, 32}) {
