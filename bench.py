@@ -111,14 +111,18 @@ def workload(cfg_name, seed, epochs_override):
     return cfg, C
 
 
-def fp64_peak_tflops():
-    """Measured DFMA peak (profiles/probe_*.json), else the nominal B200 figure."""
+def train_peak_tflops():
+    """Peak of the training kernel's exact distance element (1 F2F.F64.F32 +
+    DADD + DFMA = 3 flop): bound by the measured fp32->fp64 conversion rate
+    (profiles/probe_fp64.json) x 148 SMs x max SM clock."""
     path = os.path.join(ROOT, "profiles", "probe_fp64.json")
     if os.path.exists(path):
         with open(path) as f:
             j = json.load(f)
-        return float(j["dfma_tflops"]), "measured (profiles/probe_fp64.json)"
-    return 37.0, "nominal B200 FP64 (vendor), no measurement yet"
+        return 3.0 * j["train_element_peak_per_s"] / 1e12, ("measured F2F.F64.F32 rate "
+                                                            f"{j['f2f_per_clk_per_sm']}/clk/SM x 148 SMs x 1965 MHz "
+                                                            "x 3 flop/element (profiles/probe_fp64.json)")
+    return 3.0 * 16 * 148 * 1965e6 / 1e12, "nominal 16 F2F/clk/SM x 148 x 1965 MHz x 3 flop (no measurement file)"
 
 
 # ------------------------------------------------------------- oracle legs
@@ -263,7 +267,7 @@ def run_b200(args, rank, world, local):
     train_ms = statistics.mean(p["train_ms"] for p in phases)
     flop_per_sample = 3.0 * N * d               # fp64 distance: sub + fma per element (R10)
     achieved = flop_per_sample * T / (train_ms / 1000.0) / 1e12
-    peak, peak_src = fp64_peak_tflops()
+    peak, peak_src = train_peak_tflops()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):

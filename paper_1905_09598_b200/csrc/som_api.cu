@@ -342,12 +342,14 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
         // all-gather latency by grid size (profiles/probe_xchg_r01.json) and
         // per-CTA F2F-bound distance time: (S + 1) * d conversions at 16/clk
-        auto xchg_us = [](int G) { return G <= 32 ? 0.70 : G <= 64 ? 0.72 : G <= 128 ? 0.90 : 1.65; };
+        // (power-of-two grids measured fastest: 16-64 ~0.6-0.7 us, 128 ~0.8 us,
+        // 48/96/100/112/134/148 all slower; tools/sweep_grid.py on c2)
+        auto xchg_us = [](int G) { return G <= 32 ? 0.65 : G <= 64 ? 0.70 : G <= 128 ? 0.85 : 1.65; };
         double best = 1e30;
         int bestG = 0;
         const int gmax = std::min(h->N, h->sm_count);
-        std::vector<int> cands = {gmax, 16, 24, 32, 48, 64, 96, 128};
-        for (int S = 1; S <= 8; ++S) cands.push_back((h->N + S - 1) / S);   // balanced grids
+        std::vector<int> cands = {16, 32, 64, 128};
+        if (gmax <= 32) cands.push_back(gmax);
         for (int G : cands) {
             if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
             if (G < 1 || G > gmax) continue;
