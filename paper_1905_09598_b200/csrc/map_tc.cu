@@ -1,0 +1,418 @@
+// map_tc.cu — batch BMU mapping on the 5th-gen tensor cores (tcgen05), the
+// SOM_MAP_3XTF32 path (P:248 assignment of documents to BMUs; R20).
+//
+//   D(i, u) = |x_i|^2 - 2 x_i . w_u + |w_u|^2,  bmu1/bmu2 = two smallest (D, u)
+//
+// x . w is a true documents x units x vocabulary contraction, run as
+// 3xTF32: x = x_hi + x_lo, w = w_hi + w_lo with hi = cvt.rna.tf32(v),
+// lo = cvt.rna.tf32(v - hi) (split once, in global memory, by split_kernel),
+// and x.w ~ x_lo.w_hi + x_hi.w_lo + x_hi.w_hi accumulated in fp32 in TMEM
+// (error ~1e-7 relative, far inside the 1e-5 near-tie margin, R19).  Norms
+// are summed in fp64 by the split kernel.
+//
+// Kernel: persistent CTAs of 6 warps.  warp 0 = TMA producer (4 tiles per
+// K-block: A_hi, A_lo 128x32 fp32, B_hi, B_lo BNx32 fp32, 128B swizzle),
+// warp 1 = TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN,
+// K=8 per instruction, 12 instructions per 32-wide K-block), warps 2-5 =
+// epilogue: tcgen05.ld 32 accumulator columns at a time, D in fp32, running
+// top-2 (D, u) per document row across all unit tiles of the work item.
+// Two TMEM accumulators (2 x BN columns) let the epilogue of one unit tile
+// overlap the MMAs of the next.  A work item is (128-document block, range
+// of unit tiles); its partial top-2 keys go to the same merge kernel as the
+// exact path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "som_device.cuh"
+#include "som_internal.h"
+
+namespace som {
+
+namespace {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BN = 256;
+constexpr int TC_BK = 32;                 // fp32 elements = 128 B = one swizzle atom row
+constexpr int TC_STAGES = 2;
+constexpr int TC_THREADS = 192;
+constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;            // 16 KB
+constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;            // 32 KB
+constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
+constexpr uint32_t TMEM_COLS = 2 * TC_BN;                  // two accumulators
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled operand tile: rows of 128 B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address (16 B units)
+    d |= (uint64_t)1 << 16;                          // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+    int64_t n;        // documents
+    int N;            // units
+    int kblocks;      // padded d / 32
+    int n_tiles;      // ceil(N / BN)
+    int m_blocks;     // ceil(n / 128)
+    int nsplit;       // unit-tile ranges per document block
+    const float* xnorm;   // [n] fp32 of the fp64 |x|^2
+    const float* wnorm;   // [N] fp32 of the fp64 |w|^2
+    unsigned long long* keys;   // [nsplit][n][2]
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+              const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, const TcArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle atoms
+    unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
+    uint64_t* empty = full + TC_STAGES;
+    uint64_t* tfull = empty + TC_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per = (a.n_tiles + a.nsplit - 1) / a.nsplit;
+    const int work_items = a.m_blocks * a.nsplit;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_ahi); prefetch_tmap(&tm_alo); prefetch_tmap(&tm_bhi); prefetch_tmap(&tm_blo);
+    }
+    if (warp == 1) tmem_alloc(tmem_base_smem, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_smem;
+
+    if (warp == 0) {
+        // ===== TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
+                const int mb = wi / a.nsplit, sp = wi % a.nsplit;
+                const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
+                for (int nt = nt0; nt < nt1; ++nt) {
+                    for (int kb = 0; kb < a.kblocks; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        unsigned char* sb = smem + stage * STAGE_BYTES;
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        const int kc = kb * TC_BK;
+                        tma_load_2d(sb, &tm_ahi, &full[stage], kc, mb * TC_BM);
+                        tma_load_2d(sb + A_BYTES, &tm_alo, &full[stage], kc, mb * TC_BM);
+                        tma_load_2d(sb + 2 * A_BYTES, &tm_bhi, &full[stage], kc, nt * TC_BN);
+                        tma_load_2d(sb + 2 * A_BYTES + B_BYTES, &tm_blo, &full[stage], kc, nt * TC_BN);
+                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (one thread)
+        const uint32_t idesc = (1u << 4)                          // D format F32
+                               | (2u << 7) | (2u << 10)           // A, B format TF32
+                               | ((uint32_t)(TC_BN >> 3) << 17)   // N
+                               | ((uint32_t)(TC_BM >> 4) << 24);  // M
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t tile = 0;
+        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
+            const int sp = wi % a.nsplit;
+            const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
+            for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+                const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
+                mbar_wait(&tempty[buf], tph ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + buf * TC_BN;
+                for (int kb = 0; kb < a.kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sb = smem_u32(smem + stage * STAGE_BYTES);
+                        const uint64_t ahi = make_sdesc(sb), alo = make_sdesc(sb + A_BYTES);
+                        const uint64_t bhi = make_sdesc(sb + 2 * A_BYTES), blo = make_sdesc(sb + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 8; ++k) {
+                            const uint64_t ko = (uint64_t)((k * 32) >> 4);   // +32 B per K=8 step
+                            const uint32_t acc0 = (kb | k) != 0;
+                            mma_tf32(tmem_d, alo + ko, bhi + ko, idesc, acc0);   // small terms first
+                            mma_tf32(tmem_d, ahi + ko, blo + ko, idesc, 1u);
+                            mma_tf32(tmem_d, ahi + ko, bhi + ko, idesc, 1u);
+                        }
+                        mma_commit(&empty[stage]);                   // smem slot free when these MMAs finish
+                        if (kb == a.kblocks - 1) mma_commit(&tfull[buf]);
+                    }
+                    __syncwarp();
+                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ===== epilogue: warps 2..5 own TMEM lane quadrants (warp % 4)
+        const int q = warp & 3;
+        const int row_in_tile = q * 32 + lane;
+        uint32_t tile = 0;
+        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
+            const int mb = wi / a.nsplit, sp = wi % a.nsplit;
+            const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
+            const int64_t row = (int64_t)mb * TC_BM + row_in_tile;
+            const float xn = row < a.n ? a.xnorm[row] : 0.0f;
+            float d1 = INFINITY, d2 = INFINITY;
+            int u1 = -1, u2 = -1;
+            for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+                const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
+                mbar_wait(&tfull[buf], tph);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * TC_BN;
+#pragma unroll 1
+                for (int c = 0; c < TC_BN / 32; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    const int u0 = nt * TC_BN + c * 32;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int u = u0 + i;
+                        if (u < a.N) {
+                            // D = |x|^2 + |w|^2 - 2 x.w, clamped >= 0 (R20)
+                            float D = fmaf(-2.0f, v[i], xn + __ldg(a.wnorm + u));
+                            D = fmaxf(D, 0.0f);
+                            if (D < d1) { d2 = d1; u2 = u1; d1 = D; u1 = u; }
+                            else if (D < d2) { d2 = D; u2 = u; }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
+            }
+            if (row < a.n) {
+                unsigned long long* dst = a.keys + ((size_t)sp * a.n + row) * 2;
+                dst[0] = u1 >= 0 ? make_key(d1, u1) : ~0ull;
+                dst[1] = u2 >= 0 ? make_key(d2, u2) : ~0ull;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+// Split rows of a dense fp32 matrix into tf32 hi / lo parts (K padded to a
+// multiple of 32 with zeros) and the fp64 squared norm of each row, rounded
+// to fp32.  One warp per row; fixed reduction order (deterministic).
+__global__ void split_kernel(const float* __restrict__ src, int64_t rows, int d, int dp, float* __restrict__ hi,
+                             float* __restrict__ lo, float* __restrict__ norm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = wg; r < rows; r += nw) {
+        const float* s = src + r * d;
+        float* h = hi + r * dp;
+        float* l = lo + r * dp;
+        double acc = 0.0;
+        for (int k = lane; k < dp; k += 32) {
+            const float v = k < d ? s[k] : 0.0f;
+            uint32_t hb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+            const float hv = __uint_as_float(hb);
+            uint32_t lb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(v - hv));
+            h[k] = hv;
+            l[k] = __uint_as_float(lb);
+            acc = fma((double)v, (double)v, acc);
+        }
+        acc = warp_sum_f64(acc);
+        if (lane == 0) norm[r] = (float)acc;
+    }
+}
+
+// CSR rows -> split dense rows (zero + scatter) and norms from the non-zeros.
+__global__ void split_csr_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                 const float* __restrict__ val, int64_t r0, int64_t rows, int dp, float* __restrict__ hi,
+                                 float* __restrict__ lo, float* __restrict__ norm) {
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        float* h = hi + r * dp;
+        float* l = lo + r * dp;
+        for (int k = threadIdx.x; k < dp; k += blockDim.x) { h[k] = 0.0f; l[k] = 0.0f; }
+        __syncthreads();
+        const int64_t p0 = rowptr[r0 + r], p1 = rowptr[r0 + r + 1];
+        double acc = 0.0;
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+            const float v = val[p];
+            uint32_t hb, lb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+            const float hv = __uint_as_float(hb);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(v - hv));
+            h[col[p]] = hv;
+            l[col[p]] = __uint_as_float(lb);
+            acc = fma((double)v, (double)v, acc);
+        }
+        // block reduction (fixed order)
+        __shared__ double red[32];
+        acc = warp_sum_f64(acc);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            norm[r] = (float)t;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeFn)p;
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int dp, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)dp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)dp * 4};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int tc_padded_dim(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
+
+cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, float* norm, cudaStream_t st) {
+    const int dp = tc_padded_dim(d);
+    int blocks = (int)std::min<int64_t>((rows + 7) / 8, 148 * 16);
+    if (blocks < 1) blocks = 1;
+    split_kernel<<<blocks, 256, 0, st>>>(src, rows, d, dp, hi, lo, norm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t rows,
+                             int d, float* hi, float* lo, float* norm, cudaStream_t st) {
+    const int dp = tc_padded_dim(d);
+    int blocks = (int)std::min<int64_t>(rows, 148 * 16);
+    if (blocks < 1) return cudaSuccess;
+    split_csr_kernel<<<blocks, 256, 0, st>>>(rowptr, col, val, r0, rows, dp, hi, lo, norm);
+    return cudaGetLastError();
+}
+
+int tc_unit_tiles(int N) { return (N + TC_BN - 1) / TC_BN; }
+int tc_doc_blocks(int64_t n) { return (int)((n + TC_BM - 1) / TC_BM); }
+
+// Documents [n] split (x_hi, x_lo, xnorm) against units [N] split (w_hi,
+// w_lo, wnorm); partial top-2 keys into keys[nsplit][n][2].
+cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
+                          const float* wlo, const float* wnorm, int N, int d, int nsplit, unsigned long long* keys,
+                          int sm_count, cudaStream_t st) {
+    const int dp = tc_padded_dim(d);
+    CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+    if (!make_map(&ma_hi, xhi, n, dp, TC_BM) || !make_map(&ma_lo, xlo, n, dp, TC_BM) ||
+        !make_map(&mb_hi, whi, N, dp, TC_BN) || !make_map(&mb_lo, wlo, N, dp, TC_BN))
+        return cudaErrorInvalidValue;
+    TcArgs a;
+    a.n = n; a.N = N; a.kblocks = dp / TC_BK; a.n_tiles = tc_unit_tiles(N); a.m_blocks = tc_doc_blocks(n);
+    a.nsplit = nsplit; a.xnorm = xnorm; a.wnorm = wnorm; a.keys = keys;
+    const size_t smem = TC_STAGES * STAGE_BYTES + 1024 + 256;
+    cudaError_t e = cudaFuncSetAttribute(map_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int work = a.m_blocks * a.nsplit;
+    const int grid = std::max(1, std::min(work, sm_count));
+    map_tc_kernel<<<grid, TC_THREADS, smem, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, a);
+    return cudaGetLastError();
+}
+
+}  // namespace som

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <thread>
 #include <unordered_set>
@@ -80,6 +81,9 @@ struct som_ctx {
     DevBuf log;      // staged BMU log
     DevBuf xchg;     // per-CTA exchange slots + abort flag
     DevBuf dense;    // densified CSR chunk
+    DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp32)
+    DevBuf xsplit;   // tensor-core mapping: X chunk hi | lo | |x|^2
+    bool w_split_valid = false;
     // decay-table cache
     int64_t f_T = -1, f_t0 = -1, f_t1 = -1;
     int f_kind = -1;
@@ -181,7 +185,7 @@ extern "C" {
 
 const char* som_last_error(void) { return g_err.c_str(); }
 
-const char* som_version(void) { return "libsom 0.1 sm_100a (persistent online SOM, exact map)"; }
+const char* som_version(void) { return "libsom 0.2 sm_100a (persistent online SOM; exact fp64 and tcgen05 3xTF32 mapping)"; }
 
 som_status som_schedule_default(som_schedule* s) {
     if (!s) return fail(SOM_EINVAL, "null schedule");
@@ -237,7 +241,8 @@ void som_destroy(som_ctx* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense})
+    for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
+                      &h->wsplit, &h->xsplit})
         b->release();
     if (h->W) cudaFree(h->W);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -256,6 +261,7 @@ som_status som_set_stream(som_ctx* h, void* cuda_stream) {
 som_status som_set_weights(som_ctx* h, const float* w) {
     CHECK_HANDLE(h);
     if (!w) return fail(SOM_EINVAL, "null weights");
+    h->w_split_valid = false;
     CK(cudaMemcpyAsync(h->W, w, sizeof(float) * (size_t)h->N * h->dim, cudaMemcpyDefault, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return SOM_OK;
@@ -274,6 +280,7 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     if (!X) return fail(SOM_EINVAL, "null X");
     if (n < 1) return fail(SOM_EEMPTY, "n = 0");
     const int N = h->N;
+    h->w_split_valid = false;
     std::vector<int64_t> idx((size_t)N);
     if (N <= n) {
         // Floyd's sampling without replacement, draws from SplitMix64(seed)
@@ -324,6 +331,7 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
                                                                  (long long)t_begin, (long long)t_end, (long long)T);
     h->last_ms = 0; h->last_units = 0; h->last_launches = 0;
     if (t_end == t_begin) return SOM_OK;   // epochs = 0 or empty range: weights unchanged
+    h->w_split_valid = false;
 
     const void* Xd = nullptr;
     som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
@@ -448,15 +456,75 @@ som_status som_last_train_config(som_ctx* h, int32_t* grid, int32_t* kernel) {
 som_status som_set_map_precision(som_ctx* h, int32_t precision) {
     CHECK_HANDLE(h);
     if (precision < SOM_MAP_AUTO || precision > SOM_MAP_3XTF32) return fail(SOM_EINVAL, "unknown map precision");
-    if (precision == SOM_MAP_3XTF32) return fail(SOM_EUNSUPPORTED, "3xTF32 mapping is not built yet");
     h->map_precision = precision;
     return SOM_OK;
 }
 
 namespace {
 
+// Which mapping path serves a call (som_set_map_precision; AUTO picks the
+// tensor cores once the contraction is large enough to amortise the split).
+bool use_tc(const som_ctx* h, int64_t n) {
+    if (h->map_precision == SOM_MAP_EXACT_F64) return false;
+    if (h->map_precision == SOM_MAP_3XTF32) return true;
+    return (double)n * h->N * h->dim >= 1.0e10;
+}
+
+// W split for the tensor-core path: hi, lo (N x dp) and |w|^2, cached until W changes.
+som_status ensure_w_split(som_ctx* h, const float** whi, const float** wlo, const float** wn) {
+    const int dp = tc_padded_dim(h->dim);
+    const size_t plane = sizeof(float) * (size_t)h->N * dp;
+    if (!h->w_split_valid) {
+        CK(h->wsplit.ensure(2 * plane + sizeof(float) * (size_t)h->N));
+        char* base = (char*)h->wsplit.p;
+        CK(launch_split_rows(h->W, h->N, h->dim, (float*)base, (float*)(base + plane), (float*)(base + 2 * plane),
+                             h->stream));
+        h->w_split_valid = true;
+    }
+    char* base = (char*)h->wsplit.p;
+    *whi = (const float*)base;
+    *wlo = (const float*)(base + plane);
+    *wn = (const float*)(base + 2 * plane);
+    return SOM_OK;
+}
+
+// Tensor-core mapping of n documents whose split rows are produced chunk by
+// chunk by `fill(r0, m, hi, lo, norm)`; outputs device pointers.
+using SplitFill = std::function<cudaError_t(int64_t, int64_t, float*, float*, float*)>;
+som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, int32_t* b1, int32_t* b2, float* d2,
+                       int* launches) {
+    const float *whi, *wlo, *wn;
+    som_status st = ensure_w_split(h, &whi, &wlo, &wn);
+    if (st) return st;
+    const int dp = tc_padded_dim(h->dim);
+    const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, ((int64_t)1 << 31) / (8 * (int64_t)dp)));
+    const size_t plane = sizeof(float) * (size_t)chunk * dp;
+    CK(h->xsplit.ensure(2 * plane + sizeof(float) * (size_t)chunk));
+    char* xb = (char*)h->xsplit.p;
+    const int tiles_n = tc_unit_tiles(h->N);
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t m = std::min(chunk, n - r0);
+        CK(fill(r0, m, (float*)xb, (float*)(xb + plane), (float*)(xb + 2 * plane)));
+        const int mblocks = tc_doc_blocks(m);
+        const int nsplit = std::max(1, std::min(tiles_n, (h->sm_count + mblocks - 1) / mblocks));
+        CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)nsplit * (size_t)m));
+        CK(launch_map_tc((const float*)xb, (const float*)(xb + plane), (const float*)(xb + 2 * plane), m, whi, wlo,
+                         wn, h->N, h->dim, nsplit, (unsigned long long*)h->keys.p, h->sm_count, h->stream));
+        CK(launch_map_merge((const unsigned long long*)h->keys.p, nsplit, m, b1 + r0, b2 ? b2 + r0 : nullptr,
+                            d2 ? d2 + r0 : nullptr, h->stream));
+        *launches += 3;
+    }
+    return SOM_OK;
+}
+
 // Map n rows of the device matrix Xd into device outputs (all device).
 som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches) {
+    if (use_tc(h, n)) {
+        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
+            return launch_split_rows(Xd + r0 * h->dim, m, h->dim, hi, lo, nrm, h->stream);
+        };
+        return map_tc_rows(h, n, fill, b1, b2, d2, launches);
+    }
     const int tiles_m = map_exact_tiles_m(n);
     const int tiles_n = map_exact_tiles_n(h->N);
     int nsplit = std::max(1, std::min(tiles_n, (2 * h->sm_count + tiles_m - 1) / tiles_m));
@@ -536,6 +604,22 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
     if ((st = stage_in(h, h->xin3, val, sizeof(float) * (size_t)std::max<int64_t>(nnz, 1), &vd))) return st;
     OutStage o;
     if ((st = stage_outputs(h, n, bmu1, bmu2, d2, false, o))) return st;
+    if (use_tc(h, n)) {
+        int launches = 0;
+        CK(cudaEventRecord(h->ev0, h->stream));
+        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
+            return launch_split_csr((const int64_t*)rpd, (const int32_t*)cd, (const float*)vd, r0, m, h->dim, hi, lo,
+                                    nrm, h->stream);
+        };
+        if ((st = map_tc_rows(h, n, fill, o.b1, o.b2, o.d2, &launches))) return st;
+        CK(cudaEventRecord(h->ev1, h->stream));
+        if ((st = copy_back(h, n, bmu1, bmu2, d2, o))) return st;
+        CK(cudaStreamSynchronize(h->stream));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        h->last_ms = ms; h->last_units = n; h->last_launches = launches;
+        return SOM_OK;
+    }
     // densify in chunks of <= 1 GiB and map each chunk
     const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));
     CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim));

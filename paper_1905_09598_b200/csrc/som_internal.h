@@ -66,6 +66,18 @@ cudaError_t launch_map_merge(const unsigned long long* keys, int nsplit, int64_t
 int map_exact_tiles_n(int N);
 int map_exact_tiles_m(int64_t n);
 
+// Tensor-core (tcgen05, 3xTF32) mapping, map_tc.cu.  Operands are split into
+// tf32 hi/lo planes with K padded to tc_padded_dim(d); norms fp64 -> fp32.
+int tc_padded_dim(int d);
+int tc_unit_tiles(int N);
+int tc_doc_blocks(int64_t n);
+cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, float* norm, cudaStream_t st);
+cudaError_t launch_split_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t rows,
+                             int d, float* hi, float* lo, float* norm, cudaStream_t st);
+cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
+                          const float* wlo, const float* wnorm, int N, int d, int nsplit, unsigned long long* keys,
+                          int sm_count, cudaStream_t st);
+
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);
