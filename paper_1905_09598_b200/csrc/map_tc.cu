@@ -127,11 +127,25 @@ struct TcArgs {
     int kblocks;      // padded d / 32
     int n_tiles;      // ceil(N / BN)
     int m_blocks;     // ceil(n / 128)
-    int nsplit;       // unit-tile ranges per document block
+    int group;        // unit tiles per raster group (L2 reuse of A and B panels)
     const float* xnorm;   // [n] fp32 of the fp64 |x|^2
     const float* wnorm;   // [N] fp32 of the fp64 |w|^2
-    unsigned long long* keys;   // [nsplit][n][2]
+    unsigned long long* keys;   // [n_tiles][n][2] partial top-2 per unit tile
 };
+
+// Work item wi -> (document block, unit tile).  Grouped raster: unit tiles
+// are taken `group` at a time and, within a group, consecutive work items
+// walk the unit tiles of one document block, so the ~148 concurrently
+// running items share a few A panels (documents) and a few B panels (units)
+// in L2 instead of streaming every panel from HBM.
+__device__ __forceinline__ void work_coords(int wi, const TcArgs& a, int& mb, int& nt) {
+    const int per_group = a.m_blocks * a.group;
+    const int g = wi / per_group;
+    const int r = wi - g * per_group;
+    const int gsize = min(a.group, a.n_tiles - g * a.group);
+    mb = r / gsize;
+    nt = g * a.group + (r - mb * gsize);
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
@@ -146,8 +160,7 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
     uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per = (a.n_tiles + a.nsplit - 1) / a.nsplit;
-    const int work_items = a.m_blocks * a.nsplit;
+    const int work_items = a.m_blocks * a.n_tiles;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -169,9 +182,9 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
             int stage = 0;
             uint32_t phase = 0;
             for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
-                const int mb = wi / a.nsplit, sp = wi % a.nsplit;
-                const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
-                for (int nt = nt0; nt < nt1; ++nt) {
+                int mb, nt;
+                work_coords(wi, a, mb, nt);
+                {
                     for (int kb = 0; kb < a.kblocks; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         unsigned char* sb = smem + stage * STAGE_BYTES;
@@ -195,10 +208,8 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
         int stage = 0;
         uint32_t phase = 0;
         uint32_t tile = 0;
-        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
-            const int sp = wi % a.nsplit;
-            const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
-            for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x, ++tile) {
+            {
                 const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
                 mbar_wait(&tempty[buf], tph ^ 1);
                 tc_fence_after();
@@ -231,14 +242,14 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
         const int q = warp & 3;
         const int row_in_tile = q * 32 + lane;
         uint32_t tile = 0;
-        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x) {
-            const int mb = wi / a.nsplit, sp = wi % a.nsplit;
-            const int nt0 = sp * per, nt1 = min(a.n_tiles, nt0 + per);
+        for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x, ++tile) {
+            int mb, nt;
+            work_coords(wi, a, mb, nt);
             const int64_t row = (int64_t)mb * TC_BM + row_in_tile;
             const float xn = row < a.n ? a.xnorm[row] : 0.0f;
             float d1 = INFINITY, d2 = INFINITY;
             int u1 = -1, u2 = -1;
-            for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+            {
                 const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
                 mbar_wait(&tfull[buf], tph);
                 tc_fence_after();
@@ -265,7 +276,7 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
                 if (lane == 0) mbar_arrive(&tempty[buf]);
             }
             if (row < a.n) {
-                unsigned long long* dst = a.keys + ((size_t)sp * a.n + row) * 2;
+                unsigned long long* dst = a.keys + ((size_t)nt * a.n + row) * 2;
                 dst[0] = u1 >= 0 ? make_key(d1, u1) : ~0ull;
                 dst[1] = u2 >= 0 ? make_key(d2, u2) : ~0ull;
             }
@@ -394,10 +405,10 @@ int tc_unit_tiles(int N) { return (N + TC_BN - 1) / TC_BN; }
 int tc_doc_blocks(int64_t n) { return (int)((n + TC_BM - 1) / TC_BM); }
 
 // Documents [n] split (x_hi, x_lo, xnorm) against units [N] split (w_hi,
-// w_lo, wnorm); partial top-2 keys into keys[nsplit][n][2].
+// w_lo, wnorm); partial top-2 keys into keys[tc_unit_tiles(N)][n][2].
 cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
-                          const float* wlo, const float* wnorm, int N, int d, int nsplit, unsigned long long* keys,
-                          int sm_count, cudaStream_t st) {
+                          const float* wlo, const float* wnorm, int N, int d, unsigned long long* keys, int sm_count,
+                          cudaStream_t st) {
     const int dp = tc_padded_dim(d);
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     if (!make_map(&ma_hi, xhi, n, dp, TC_BM) || !make_map(&ma_lo, xlo, n, dp, TC_BM) ||
@@ -405,11 +416,22 @@ cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm
         return cudaErrorInvalidValue;
     TcArgs a;
     a.n = n; a.N = N; a.kblocks = dp / TC_BK; a.n_tiles = tc_unit_tiles(N); a.m_blocks = tc_doc_blocks(n);
-    a.nsplit = nsplit; a.xnorm = xnorm; a.wnorm = wnorm; a.keys = keys;
+    a.xnorm = xnorm; a.wnorm = wnorm; a.keys = keys;
+    // group size: minimise panel re-streaming for ~sm_count concurrent items,
+    // (n_tiles/b)|A| + (m_blocks/(sm/b))|B| with |A| ~ n, |B| ~ N
+    {
+        double best = 1e300;
+        a.group = a.n_tiles;
+        for (int b = 1; b <= a.n_tiles; ++b) {
+            const double conc_m = std::max(1.0, (double)sm_count / b);
+            const double cost = (double)a.n_tiles / b * (double)n + (double)a.m_blocks / conc_m * (double)N;
+            if (cost < best) { best = cost; a.group = b; }
+        }
+    }
     const size_t smem = TC_STAGES * STAGE_BYTES + 1024 + 256;
     cudaError_t e = cudaFuncSetAttribute(map_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int work = a.m_blocks * a.nsplit;
+    const int work = a.m_blocks * a.n_tiles;
     const int grid = std::max(1, std::min(work, sm_count));
     map_tc_kernel<<<grid, TC_THREADS, smem, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, a);
     return cudaGetLastError();

@@ -497,20 +497,19 @@ som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, int32_t* b1
     som_status st = ensure_w_split(h, &whi, &wlo, &wn);
     if (st) return st;
     const int dp = tc_padded_dim(h->dim);
-    const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, ((int64_t)1 << 31) / (8 * (int64_t)dp)));
+    // split-X chunk: up to 8 GiB of hi/lo planes (large chunks keep B panels hot)
+    const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, ((int64_t)8 << 30) / (8 * (int64_t)dp)));
     const size_t plane = sizeof(float) * (size_t)chunk * dp;
     CK(h->xsplit.ensure(2 * plane + sizeof(float) * (size_t)chunk));
     char* xb = (char*)h->xsplit.p;
     const int tiles_n = tc_unit_tiles(h->N);
+    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles_n * (size_t)chunk));
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t m = std::min(chunk, n - r0);
         CK(fill(r0, m, (float*)xb, (float*)(xb + plane), (float*)(xb + 2 * plane)));
-        const int mblocks = tc_doc_blocks(m);
-        const int nsplit = std::max(1, std::min(tiles_n, (h->sm_count + mblocks - 1) / mblocks));
-        CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)nsplit * (size_t)m));
         CK(launch_map_tc((const float*)xb, (const float*)(xb + plane), (const float*)(xb + 2 * plane), m, whi, wlo,
-                         wn, h->N, h->dim, nsplit, (unsigned long long*)h->keys.p, h->sm_count, h->stream));
-        CK(launch_map_merge((const unsigned long long*)h->keys.p, nsplit, m, b1 + r0, b2 ? b2 + r0 : nullptr,
+                         wn, h->N, h->dim, (unsigned long long*)h->keys.p, h->sm_count, h->stream));
+        CK(launch_map_merge((const unsigned long long*)h->keys.p, tiles_n, m, b1 + r0, b2 ? b2 + r0 : nullptr,
                             d2 ? d2 + r0 : nullptr, h->stream));
         *launches += 3;
     }

@@ -75,8 +75,8 @@ cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, 
 cudaError_t launch_split_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t rows,
                              int d, float* hi, float* lo, float* norm, cudaStream_t st);
 cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
-                          const float* wlo, const float* wnorm, int N, int d, int nsplit, unsigned long long* keys,
-                          int sm_count, cudaStream_t st);
+                          const float* wlo, const float* wnorm, int N, int d, unsigned long long* keys, int sm_count,
+                          cudaStream_t st);
 
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
