@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--epochs", type=int, default=None, help="override epochs (diagnostics only)")
     p.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--map-docs", type=int, default=200000, help="documents in the c5-shaped mapping leg (0 = skip)")
     return p.parse_args()
 
 
@@ -123,6 +124,57 @@ def train_peak_tflops():
                                                             f"{j['f2f_per_clk_per_sm']}/clk/SM x 148 SMs x 1965 MHz "
                                                             "x 3 flop/element (profiles/probe_fp64.json)")
     return 3.0 * 16 * 148 * 1965e6 / 1e12, "nominal 16 F2F/clk/SM x 148 x 1965 MHz x 3 flop (no measurement file)"
+
+
+def tf32_peak_tflops():
+    """Dense TF32 peak: the measured bf16 cuBLAS peak (MEASURED_PEAKS.json,
+    burst) x the nominal tf32/bf16 ratio 1.1/2.25 (B200_PROFILING.md)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        return bf16 * 1.1 / 2.25, f"measured bf16 {bf16} TFLOP/s x 1.1/2.25 (MEASURED_PEAKS.json)"
+    return 1590.0 * 1.1 / 2.25, "fallback bf16 1590 TFLOP/s x 1.1/2.25 (B200_PROFILING.md)"
+
+
+def mapping_leg(som, torch, args, local, seed):
+    """Batch BMU mapping docs/s on a c5-shaped sample (BASELINE.json configs[4]:
+    100x100 map, 20k terms, CSR documents; the full 10M-document job is the
+    doc-sharded multi-GPU case) through som_map_csr on the tcgen05 path."""
+    cfg = CONFIGS["c5"]
+    n, d, N = args.map_docs, cfg["d"], cfg["rows"] * cfg["cols"]
+    C = bank_corpus(n, d, seed=seed + 500)
+    Wsrc = bank_corpus(N, d, seed=seed + 501).dense()
+    W = (0.5 * Wsrc + 0.5 / np.sqrt(d)).astype(np.float32)
+    del Wsrc
+    mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+    som.som_set_stream(mm.h, torch.cuda.current_stream())
+    mm.set_weights(torch.from_numpy(W).cuda())
+    som.som_set_map_precision(mm.h, som.SOM_MAP_3XTF32)
+    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
+    b1 = torch.empty(n, dtype=torch.int32, device="cuda")
+    b2 = torch.empty(n, dtype=torch.int32, device="cuda")
+    d1 = torch.empty(n, dtype=torch.float32, device="cuda")
+    som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)          # warm-up (W split, scratch)
+    times, kern = [], []
+    for _ in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)
+        ms, _, launches = som.som_last_stats(mm.h)
+        times.append(ms)
+        kern.append(launches)
+    ms = statistics.mean(times)
+    flop = 2.0 * n * N * d
+    peak, src = tf32_peak_tflops()
+    executed = 3.0 * flop / (ms / 1000.0) / 1e12
+    mm.close()
+    return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms",
+            "docs_per_s": n / (ms / 1000.0), "ms": ms, "launches": kern[-1],
+            "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
+                         "achieved": executed, "peak": peak, "unit": "TFLOP/s", "frac": executed / peak,
+                         "peak_source": src,
+                         "work": "3 x 2*n*N*d executed TF32 flop per call (3xTF32 split), incl. CSR split + merge",
+                         "algorithmic_fp32_tflops": flop / (ms / 1000.0) / 1e12}}
 
 
 # ------------------------------------------------------------- oracle legs
@@ -274,6 +326,11 @@ def run_b200(args, rank, world, local):
         with open(tpath) as f:
             traffic = json.load(f).get("bytes_per_launch")
 
+    g_used, k_used = som.som_last_train_config(m.h)
+    kname = {0: "som_train_kernel (W global)", 1: "som_train_kernel (W smem)",
+             2: "som_train_reg_kernel (W registers)"}.get(k_used, "?")
+    mapping = mapping_leg(som, torch, args, local, seed) if args.map_docs > 0 else None
+
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
@@ -307,7 +364,8 @@ def run_b200(args, rank, world, local):
         "e2e": {"value": world * T / (float(e2e_t.item()) / 1000.0), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "alu", "kernel": "som_train_kernel", "achieved": achieved, "peak": peak,
+        "mapping": mapping,
+        "roofline": {"bound": "alu", "kernel": f"{kname}, G={g_used}", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
                      "work": "3*N*d fp64 flop per sample (difference + fused square-accumulate)"},
