@@ -136,6 +136,32 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * kernel 0 = W in global memory, 1 = W in shared memory, 2 = W in registers. */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
+/* ---- Neuron sharding: online training of one map across
+ * `world` GPUs (one process or handle per rank).  Rank r holds the units
+ * u = r + world*l (cyclic, so the shrinking neighbourhood stays spread);
+ * every rank passes the same full X and seed (the sampler is counter-based,
+ * so x_t needs no communication).  Each step, after the in-GPU argmin, the
+ * rank's winner (8 bytes) is written into every rank's mailbox in peer
+ * memory (NVLink) by the training kernel itself and the global minimum
+ * taken — results are identical to world = 1.
+ *   som_comm_init           switch the handle to rank/world (W re-zeroed;
+ *                           set/get/init weights keep using the FULL map,
+ *                           only this rank's rows are read/written)
+ *   som_comm_mailbox_ipc    64-byte cudaIpcMemHandle of this rank's mailbox
+ *   som_comm_set_peers_ipc  world x 64 bytes of handles (all ranks; own
+ *                           entry ignored), opened with cudaIpcOpenMemHandle
+ *   som_comm_set_peers_dev  world device pointers (same-process ranks)
+ * Sharded som_train_online calls are collective: every rank calls with the
+ * same arguments, and callers barrier between consecutive calls (the
+ * mailbox is cleared at the end of each call).  Mapping, errors and the
+ * U-matrix are not served by a sharded handle (SOM_EUNSUPPORTED). */
+som_status som_comm_init(som_ctx *h, int32_t rank, int32_t world);
+som_status som_comm_local_units(som_ctx *h, int32_t *n_local);
+som_status som_comm_mailbox_ipc(som_ctx *h, uint8_t *handle64);
+som_status som_comm_set_peers_ipc(som_ctx *h, const uint8_t *handles);
+som_status som_comm_set_peers_dev(som_ctx *h, void *const *mailboxes);
+som_status som_comm_mailbox_ptr(som_ctx *h, void **mailbox);
+
 /* Phase trace of the register-resident training kernel (profiling aid):
  * device_buf (device memory, 148 * steps * 8 uint64, layout [CTA][step][8])
  * receives %globaltimer (ns) at 8 phase boundaries of the first `steps`

@@ -58,7 +58,12 @@ struct DevBuf {
 
 struct som_ctx {
     int rows = 0, cols = 0, dim = 0, topo = 0, device = 0;
-    int N = 0;
+    int N = 0;                // units of the map (global)
+    int NL = 0;               // units held by this handle (N unless neuron-sharded)
+    int rank = 0, world = 1;  // neuron sharding: units u = rank + world * l
+    unsigned long long* mail = nullptr;            // own cross-rank mailbox [2][world]
+    unsigned long long* peer_mail[kMaxRanks] = {}; // every rank's mailbox (own included)
+    bool peer_ipc[kMaxRanks] = {};                 // opened with cudaIpcOpenMemHandle
     float* W = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
@@ -217,6 +222,7 @@ som_status som_create(int32_t rows, int32_t cols, int32_t dim, int32_t topology,
     som_ctx* h = new som_ctx();
     h->rows = rows; h->cols = cols; h->dim = dim; h->topo = topology; h->device = device;
     h->N = rows * cols;
+    h->NL = h->N;
     h->sm_count = prop.multiProcessorCount;
     h->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
     auto bad = [&](cudaError_t err, const char* what) {
@@ -245,6 +251,9 @@ void som_destroy(som_ctx* h) {
                       &h->wsplit, &h->xsplit})
         b->release();
     if (h->W) cudaFree(h->W);
+    for (int p = 0; p < kMaxRanks; ++p)
+        if (h->peer_ipc[p] && h->peer_mail[p]) cudaIpcCloseMemHandle(h->peer_mail[p]);
+    if (h->mail) cudaFree(h->mail);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -258,11 +267,16 @@ som_status som_set_stream(som_ctx* h, void* cuda_stream) {
     return SOM_OK;
 }
 
+// The caller always passes the FULL N x dim map.  A neuron-sharded handle
+// keeps rows u = rank + world*l (strided 2-D copies); other rows of the
+// caller's buffer are left untouched by som_get_weights.
 som_status som_set_weights(som_ctx* h, const float* w) {
     CHECK_HANDLE(h);
     if (!w) return fail(SOM_EINVAL, "null weights");
     h->w_split_valid = false;
-    CK(cudaMemcpyAsync(h->W, w, sizeof(float) * (size_t)h->N * h->dim, cudaMemcpyDefault, h->stream));
+    const size_t rowb = sizeof(float) * (size_t)h->dim;
+    CK(cudaMemcpy2DAsync(h->W, rowb, w + (size_t)h->rank * h->dim, rowb * h->world, rowb, (size_t)h->NL,
+                         cudaMemcpyDefault, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return SOM_OK;
 }
@@ -270,7 +284,9 @@ som_status som_set_weights(som_ctx* h, const float* w) {
 som_status som_get_weights(som_ctx* h, float* w) {
     CHECK_HANDLE(h);
     if (!w) return fail(SOM_EINVAL, "null weights");
-    CK(cudaMemcpyAsync(w, h->W, sizeof(float) * (size_t)h->N * h->dim, cudaMemcpyDefault, h->stream));
+    const size_t rowb = sizeof(float) * (size_t)h->dim;
+    CK(cudaMemcpy2DAsync(w + (size_t)h->rank * h->dim, rowb * h->world, h->W, rowb, rowb, (size_t)h->NL,
+                         cudaMemcpyDefault, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return SOM_OK;
 }
@@ -296,15 +312,20 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     } else {
         for (int u = 0; u < N; ++u) idx[(size_t)u] = (int64_t)mulhi_host(splitmix64_at(seed, u), (uint64_t)n);
     }
+    // a neuron-sharded handle keeps the draws of its own units
+    std::vector<int64_t> mine((size_t)h->NL);
+    for (int l = 0; l < h->NL; ++l) mine[(size_t)l] = idx[(size_t)h->rank + (size_t)h->world * l];
+    const int NL = h->NL;
     const size_t rowb = sizeof(float) * (size_t)h->dim;
     if (is_device_ptr(X)) {
-        CK(h->keys.ensure(sizeof(int64_t) * (size_t)N));
-        CK(cudaMemcpyAsync(h->keys.p, idx.data(), sizeof(int64_t) * (size_t)N, cudaMemcpyHostToDevice, h->stream));
-        CK(launch_gather_rows(X, (const int64_t*)h->keys.p, N, h->dim, h->W, h->stream));
+        CK(h->keys.ensure(sizeof(int64_t) * (size_t)NL));
+        CK(cudaMemcpyAsync(h->keys.p, mine.data(), sizeof(int64_t) * (size_t)NL, cudaMemcpyHostToDevice, h->stream));
+        CK(launch_gather_rows(X, (const int64_t*)h->keys.p, NL, h->dim, h->W, h->stream));
     } else {
-        std::vector<float> rowsbuf((size_t)N * h->dim);
-        for (int u = 0; u < N; ++u) std::memcpy(rowsbuf.data() + (size_t)u * h->dim, X + idx[(size_t)u] * h->dim, rowb);
-        CK(cudaMemcpyAsync(h->W, rowsbuf.data(), rowb * (size_t)N, cudaMemcpyHostToDevice, h->stream));
+        std::vector<float> rowsbuf((size_t)NL * h->dim);
+        for (int l = 0; l < NL; ++l)
+            std::memcpy(rowsbuf.data() + (size_t)l * h->dim, X + mine[(size_t)l] * h->dim, rowb);
+        CK(cudaMemcpyAsync(h->W, rowsbuf.data(), rowb * (size_t)NL, cudaMemcpyHostToDevice, h->stream));
     }
     CK(cudaStreamSynchronize(h->stream));
     return SOM_OK;
@@ -340,7 +361,13 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
 
     TrainArgs a{};
     a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
-    a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->N;
+    a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->NL;
+    a.rank = h->rank; a.world = h->world;
+    for (int p = 0; p < kMaxRanks; ++p) a.mail[p] = h->peer_mail[p];
+    if (h->world > 1) {
+        for (int p = 0; p < h->world; ++p)
+            if (!h->peer_mail[p]) return fail(SOM_ESTATE, "neuron sharding: peer mailboxes not set (som_comm_set_peers_*)");
+    }
     a.x_vec4 = (h->dim % 4 == 0) && ((uintptr_t)Xd % 16 == 0);
     // launch geometry.  Register-resident kernel when a CTA's share of W fits
     // the register file: G minimises (all-gather latency + fp64 distance
@@ -355,13 +382,13 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
         auto xchg_us = [](int G) { return G <= 32 ? 0.65 : G <= 64 ? 0.70 : G <= 128 ? 0.85 : 1.65; };
         double best = 1e30;
         int bestG = 0;
-        const int gmax = std::min(h->N, h->sm_count);
+        const int gmax = std::min(h->NL, h->sm_count);
         std::vector<int> cands = {16, 32, 64, 128};
         if (gmax <= 32) cands.push_back(gmax);
         for (int G : cands) {
             if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
             if (G < 1 || G > gmax) continue;
-            const int S = (h->N + G - 1) / G;
+            const int S = (h->NL + G - 1) / G;
             if (!train_reg_supported(S, h->dim)) continue;
             const double est = xchg_us(G) + (double)(S + 1) * h->dim / (16.0 * 1965.0);
             if (est < best) { best = est; bestG = G; }
@@ -371,10 +398,10 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     if (h->train_mode == SOM_TRAIN_W_REGISTERS && !use_reg)
         return fail(SOM_EUNSUPPORTED, "map share per CTA does not fit registers (or d %% 4 != 0)");
     if (!use_reg) {
-        a.G = std::min(h->N, h->sm_count);
+        a.G = std::min(h->NL, h->sm_count);
         if (h->train_grid > 0) a.G = std::min(a.G, h->train_grid);
     }
-    a.S = (h->N + a.G - 1) / a.G;
+    a.S = (h->NL + a.G - 1) / a.G;
     a.t0 = t_begin; a.t1 = t_end; a.seed = seed;
     a.f_tab = (const double*)h->ftab.p;
     a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
@@ -415,11 +442,96 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     CK(cudaMemcpy(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost));
     if (abort_flag) {
         h->poisoned = true;
-        return fail(SOM_ECUDA, "training exchange timed out (a CTA stopped publishing its BMU candidate)");
+        return fail(SOM_ECUDA, "training exchange timed out (a CTA or rank stopped publishing its BMU candidate)");
+    }
+    // neuron sharding: clear the own mailbox so the next call's tags cannot
+    // match stale entries (callers barrier between sharded calls)
+    if (h->world > 1) {
+        CK(cudaMemsetAsync(h->mail, 0, sizeof(unsigned long long) * 2 * (size_t)h->world, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
     }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_ms = ms; h->last_units = steps; h->last_launches = 1;
+    return SOM_OK;
+}
+
+som_status som_comm_init(som_ctx* h, int32_t rank, int32_t world) {
+    CHECK_HANDLE(h);
+    if (world < 1 || world > kMaxRanks) return fail(SOM_EINVAL, "world must be in [1, %d]", kMaxRanks);
+    if (rank < 0 || rank >= world) return fail(SOM_EINVAL, "rank out of range");
+    if (world > h->N) return fail(SOM_EINVAL, "more ranks than map units");
+    const int NL = (h->N - rank + world - 1) / world;
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->W) CK(cudaFree(h->W));
+    h->W = nullptr;
+    CK(cudaMalloc(&h->W, sizeof(float) * (size_t)NL * h->dim));
+    CK(cudaMemsetAsync(h->W, 0, sizeof(float) * (size_t)NL * h->dim, h->stream));
+    for (int p = 0; p < kMaxRanks; ++p) {
+        if (h->peer_ipc[p] && h->peer_mail[p]) cudaIpcCloseMemHandle(h->peer_mail[p]);
+        h->peer_ipc[p] = false;
+        h->peer_mail[p] = nullptr;
+    }
+    if (h->mail) CK(cudaFree(h->mail));
+    h->mail = nullptr;
+    // one 2 MiB-aligned allocation of its own so its IPC handle maps nothing else
+    CK(cudaMalloc(&h->mail, 2u << 20));
+    CK(cudaMemsetAsync(h->mail, 0, 2u << 20, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->rank = rank;
+    h->world = world;
+    h->NL = NL;
+    h->peer_mail[rank] = h->mail;
+    h->w_split_valid = false;
+    return SOM_OK;
+}
+
+som_status som_comm_local_units(som_ctx* h, int32_t* n_local) {
+    if (!h || !n_local) return fail(SOM_EINVAL, "null argument");
+    *n_local = h->NL;
+    return SOM_OK;
+}
+
+som_status som_comm_mailbox_ipc(som_ctx* h, uint8_t* handle64) {
+    CHECK_HANDLE(h);
+    if (!handle64) return fail(SOM_EINVAL, "null handle buffer");
+    if (!h->mail) return fail(SOM_ESTATE, "som_comm_init first");
+    cudaIpcMemHandle_t ih;
+    CK(cudaIpcGetMemHandle(&ih, h->mail));
+    std::memcpy(handle64, &ih, sizeof(ih));
+    return SOM_OK;
+}
+
+som_status som_comm_set_peers_ipc(som_ctx* h, const uint8_t* handles) {
+    CHECK_HANDLE(h);
+    if (!handles) return fail(SOM_EINVAL, "null handles");
+    if (!h->mail) return fail(SOM_ESTATE, "som_comm_init first");
+    for (int p = 0; p < h->world; ++p) {
+        if (p == h->rank) continue;
+        cudaIpcMemHandle_t ih;
+        std::memcpy(&ih, handles + 64 * (size_t)p, sizeof(ih));
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess));
+        h->peer_mail[p] = (unsigned long long*)ptr;
+        h->peer_ipc[p] = true;
+    }
+    return SOM_OK;
+}
+
+som_status som_comm_set_peers_dev(som_ctx* h, void* const* mailboxes) {
+    CHECK_HANDLE(h);
+    if (!mailboxes) return fail(SOM_EINVAL, "null mailboxes");
+    if (!h->mail) return fail(SOM_ESTATE, "som_comm_init first");
+    for (int p = 0; p < h->world; ++p) {
+        if (!mailboxes[p]) return fail(SOM_EINVAL, "null mailbox for rank %d", p);
+        h->peer_mail[p] = (unsigned long long*)mailboxes[p];
+    }
+    return SOM_OK;
+}
+
+som_status som_comm_mailbox_ptr(som_ctx* h, void** mailbox) {
+    if (!h || !mailbox) return fail(SOM_EINVAL, "null argument");
+    *mailbox = h->mail;
     return SOM_OK;
 }
 
@@ -564,6 +676,8 @@ som_status copy_back(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float*
 
 som_status som_map(som_ctx* h, const float* X, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2) {
     CHECK_HANDLE(h);
+    if (h->world > 1)
+        return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
     if (n < 0) return fail(SOM_EINVAL, "n < 0");
     if (n == 0) return SOM_OK;   // S:240 empty matrix -> empty result
     if (!X || !bmu1) return fail(SOM_EINVAL, "null X or bmu1");
@@ -587,6 +701,8 @@ som_status som_map(som_ctx* h, const float* X, int64_t n, int32_t* bmu1, int32_t
 som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
                        int32_t* bmu1, int32_t* bmu2, float* d2) {
     CHECK_HANDLE(h);
+    if (h->world > 1)
+        return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
     if (n < 0) return fail(SOM_EINVAL, "n < 0");
     if (n == 0) return SOM_OK;
     if (!rowptr || !col || !val || !bmu1) return fail(SOM_EINVAL, "null CSR array or bmu1");
@@ -644,6 +760,8 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
 
 som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double* te) {
     CHECK_HANDLE(h);
+    if (h->world > 1)
+        return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
     if (!X) return fail(SOM_EINVAL, "null X");
     if (n < 1) return fail(SOM_EEMPTY, "n = 0: errors need data");
     const void* Xd = nullptr;
@@ -688,6 +806,8 @@ som_status som_topographic_error(som_ctx* h, const float* X, int64_t n, double* 
 
 som_status som_umatrix(som_ctx* h, float* U) {
     CHECK_HANDLE(h);
+    if (h->world > 1)
+        return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
     if (!U) return fail(SOM_EINVAL, "null U");
     const bool dev = is_device_ptr(U);
     float* Ud = U;

@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "som_device.cuh"
+
 namespace som {
 
 constexpr int kTrainThreads = 512;                 // 16 warps per persistent CTA
@@ -35,10 +37,84 @@ struct TrainArgs {
     int x_vec4;                // 1: X rows are 16-byte aligned (d % 4 == 0)
     unsigned long long* trace; // nullable: [G][trace_steps][kTracePhases] globaltimer (ns) per CTA
     int trace_steps;
+    // neuron sharding: this launch holds the N local units
+    // l = 0..N-1 of global units u = rank + world * l; after the in-GPU
+    // exchange, CTA 0 publishes the local winner into mail[p][t&1][rank] of
+    // every rank p (peer memory over NVLink) and all CTAs poll mail[rank].
+    int rank, world;
+    unsigned long long* mail[8];
 };
 
 constexpr int kTracePhases = 8;
+constexpr int kMaxRanks = 8;
+constexpr unsigned kSpinLimitX = 1u << 24;
 
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Per-step global argmin (warp 0 of every CTA; R9), in two calls so
+// the caller can overlap work with the wait.  key: this CTA's min (D bits |
+// global unit << 8).  Level 1: tagged all-gather over the G CTAs of this GPU
+// (slots double-buffered by t&1: a CTA can only overwrite parity p after
+// every CTA published the step in between, i.e. after all reads of parity
+// p).  Level 2 (world > 1): CTA 0 forwards the GPU winner to every rank's
+// mailbox (system-scope stores into peer memory); all CTAs poll their own
+// mailbox.  Bounded spins: on timeout or a raised abort flag the wait
+// returns with *stop = 1 (the host reports SOM_ECUDA, never hangs).
+__device__ __forceinline__ unsigned long long xchg_tag(int64_t t) { return 0x80ull | (unsigned long long)(t & 0x7F); }
+
+__device__ __forceinline__ void xchg_publish(const TrainArgs& a, unsigned long long key, int64_t t, int b, int lane) {
+    if (lane == 0) st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.G + b, (key & ~0xFFull) | xchg_tag(t));
+}
+
+__device__ __forceinline__ bool xchg_should_stop(const TrainArgs& a, unsigned& spins, int lane) {
+    if ((++spins & 255u) != 0u) return false;
+    const bool s = spins > kSpinLimitX || ld_relaxed_u32(a.abort_flag) != 0u;
+    if (__any_sync(0xffffffffu, s)) {
+        if (lane == 0) atomicExch(a.abort_flag, 1u);
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int64_t t, int b, int lane, int* stop) {
+    const unsigned long long tag = xchg_tag(t);
+    const unsigned long long* slots = a.xchg + (size_t)(t & 1) * a.G;
+    unsigned long long gmin = 0;
+    unsigned spins = 0;
+    for (;;) {
+        unsigned long long m = ~0ull;
+        bool ok = true;
+        for (int j = lane; j < a.G; j += 32) {
+            const unsigned long long v = ld_relaxed_u64(slots + j);
+            ok &= (v & 0xFFull) == tag;
+            m = umin64(m, v);
+        }
+        if (__all_sync(0xffffffffu, ok)) { gmin = warp_min_u64(m); break; }
+        if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
+    }
+    if (a.world <= 1) return gmin;
+    const size_t par = (size_t)(t & 1) * a.world;
+    if (b == 0 && lane < a.world) st_relaxed_sys_u64(a.mail[lane] + par + a.rank, gmin);
+    const unsigned long long* mine = a.mail[a.rank] + par;
+    spins = 0;
+    for (;;) {
+        unsigned long long v = ~0ull;
+        bool ok = true;
+        if (lane < a.world) { v = ld_relaxed_sys_u64(mine + lane); ok = (v & 0xFFull) == tag; }
+        if (__all_sync(0xffffffffu, ok)) return warp_min_u64(v);
+        if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
+    }
+}
+
+// global unit index of local unit l
+__device__ __forceinline__ int global_unit(const TrainArgs& a, int l) { return a.rank + a.world * l; }
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -30,7 +30,6 @@ namespace som {
 
 namespace {
 
-constexpr unsigned kSpinLimit = 1u << 24;
 
 struct Smem {
     float* xs;        // [2][dimp] x ring (t even / odd)
@@ -208,36 +207,15 @@ __global__ void __launch_bounds__(kTrainThreads, 1) som_train_kernel(const Train
                 double tot = 0.0;
 #pragma unroll
                 for (int w = 0; w < kTrainWarps; ++w) tot += sm.part[s * kTrainWarps + w];
-                best = umin64(best, make_key((float)tot, b + s * G));
+                best = umin64(best, make_key((float)tot, global_unit(a, b + s * G)));
             }
             best = warp_min_u64(best);
 
-            // exchange: publish (key | tag) into slot [t&1][b], gather all G
-            const unsigned long long tag = 0x80ull | (unsigned long long)(t & 0x7F);
-            unsigned long long* slots = a.xchg + (size_t)(t & 1) * G;
-            if (lane == 0) st_relaxed_u64(slots + b, (best & ~0xFFull) | tag);
-            unsigned long long gmin;
-            unsigned spins = 0;
-            for (;;) {
-                unsigned long long m = ~0ull;
-                bool ok = true;
-                for (int j = lane; j < G; j += 32) {
-                    unsigned long long v = ld_relaxed_u64(slots + j);
-                    ok &= (v & 0xFFull) == tag;
-                    m = umin64(m, v);
-                }
-                if (__all_sync(0xffffffffu, ok)) { gmin = warp_min_u64(m); break; }
-                ++spins;
-                if ((spins & 255u) == 0u) {
-                    // bounded spin: a lost peer fails the call instead of hanging it
-                    bool stop = spins > kSpinLimit || ld_relaxed_u32(a.abort_flag) != 0u;
-                    if (__any_sync(0xffffffffu, stop)) {
-                        if (lane == 0) { atomicExch(a.abort_flag, 1u); s_abort = 1; }
-                        gmin = 0;  // results are discarded by the host
-                        break;
-                    }
-                }
-            }
+            // exchange (in-GPU all-gather, then across ranks when sharded)
+            xchg_publish(a, best, t, b, lane);
+            int stop = 0;
+            const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
+            if (stop && lane == 0) s_abort = 1;
             const int c = key_unit(gmin);
             c_last = c;
             if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
@@ -250,7 +228,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) som_train_kernel(const Train
             const double two_s2 = 2.0 * sigma * sigma;
             const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
             for (int s = lane; s < Sb; s += 32) {
-                const double g2 = lattice_g2(a.cols, a.topo, b + s * G, c);
+                const double g2 = lattice_g2(a.cols, a.topo, global_unit(a, b + s * G), c);
                 const bool up = g2 <= r2;
                 sm.upd[s] = up ? 1 : 0;
                 sm.hs[s] = up ? (float)(alpha * exp(-g2 / two_s2)) : 0.0f;

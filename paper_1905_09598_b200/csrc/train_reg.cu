@@ -24,7 +24,6 @@ namespace som {
 
 namespace {
 
-constexpr unsigned kSpinLimitR = 1u << 24;
 constexpr int NT = kTrainThreads;
 constexpr int NW = kTrainWarps;
 
@@ -76,7 +75,11 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     if (threadIdx.x == 0) s_abort = 0;
     // lattice coordinates of unit s = lane (warp 0, lanes < Sb)
     int my_i = 0, my_j = 0;
-    if (lane < SMAX && lane < Sb) { const int u = b + lane * G; my_i = u / a.cols; my_j = u - my_i * a.cols; }
+    if (lane < SMAX && lane < Sb) {
+        const int u = global_unit(a, b + lane * G);
+        my_i = u / a.cols;
+        my_j = u - my_i * a.cols;
+    }
 
     auto issue_x = [&](int64_t t) {
         if (t < a.t1) {
@@ -164,36 +167,18 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
                 double tot = 0.0;
 #pragma unroll
                 for (int w8 = 0; w8 < NW; ++w8) tot += part[w8][lane];
-                key = make_key((float)tot, b + lane * G);
+                key = make_key((float)tot, global_unit(a, b + lane * G));
             }
 #pragma unroll
             for (int o = SMAX / 2; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
             key = __shfl_sync(0xffffffffu, key, 0);
 
-            const unsigned long long tag = 0x80ull | (unsigned long long)(t & 0x7F);
-            unsigned long long* slots = a.xchg + (size_t)(t & 1) * G;
-            if (lane == 0) st_relaxed_u64(slots + b, (key & ~0xFFull) | tag);
+            xchg_publish(a, key, t, b, lane);
             TRACE(3);
             shift_x(t + 1);                       // hidden behind the poll
-            unsigned long long gmin = 0;
-            unsigned spins = 0;
-            for (;;) {
-                unsigned long long m = ~0ull;
-                bool ok = true;
-                for (int j = lane; j < G; j += 32) {
-                    const unsigned long long v = ld_relaxed_u64(slots + j);
-                    ok &= (v & 0xFFull) == tag;
-                    m = umin64(m, v);
-                }
-                if (__all_sync(0xffffffffu, ok)) { gmin = warp_min_u64(m); break; }
-                if ((++spins & 255u) == 0u) {
-                    const bool stop = spins > kSpinLimitR || ld_relaxed_u32(a.abort_flag) != 0u;
-                    if (__any_sync(0xffffffffu, stop)) {
-                        if (lane == 0) { atomicExch(a.abort_flag, 1u); s_abort = 1; }
-                        break;
-                    }
-                }
-            }
+            int stop = 0;
+            const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
+            if (stop && lane == 0) s_abort = 1;
             const int c = key_unit(gmin);
             TRACE(4);
             if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;

@@ -44,7 +44,8 @@ _lib = None
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
            "som_init_random", "som_train_online", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
            "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
-           "som_last_stats", "som_last_error", "som_version"]
+           "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
+           "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
 
 
 def lib():
@@ -76,6 +77,12 @@ def lib():
         "som_umatrix": [P, P],
         "som_set_stream": [P, P],
         "som_last_stats": [P, P, P, P],
+        "som_comm_init": [P, i32, i32],
+        "som_comm_local_units": [P, P],
+        "som_comm_mailbox_ipc": [P, P],
+        "som_comm_set_peers_ipc": [P, P],
+        "som_comm_set_peers_dev": [P, P],
+        "som_comm_mailbox_ptr": [P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -219,6 +226,39 @@ def som_last_stats(h) -> tuple[float, int, int]:
     ms, units, launches = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int32()
     _check(lib().som_last_stats(h, ctypes.byref(ms), ctypes.byref(units), ctypes.byref(launches)))
     return ms.value, units.value, launches.value
+
+
+def som_comm_init(h, rank: int, world: int) -> None:
+    _check(lib().som_comm_init(h, rank, world))
+
+
+def som_comm_local_units(h) -> int:
+    v = ctypes.c_int32()
+    _check(lib().som_comm_local_units(h, ctypes.byref(v)))
+    return v.value
+
+
+def som_comm_mailbox_ipc(h) -> bytes:
+    buf = (ctypes.c_uint8 * 64)()
+    _check(lib().som_comm_mailbox_ipc(h, buf))
+    return bytes(buf)
+
+
+def som_comm_set_peers_ipc(h, handles: list[bytes]) -> None:
+    blob = b"".join(handles)
+    buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _check(lib().som_comm_set_peers_ipc(h, buf))
+
+
+def som_comm_set_peers_dev(h, mailboxes: list[int]) -> None:
+    arr = (ctypes.c_void_p * len(mailboxes))(*mailboxes)
+    _check(lib().som_comm_set_peers_dev(h, arr))
+
+
+def som_comm_mailbox_ptr(h) -> int:
+    v = ctypes.c_void_p()
+    _check(lib().som_comm_mailbox_ptr(h, ctypes.byref(v)))
+    return v.value or 0
 
 
 def som_last_error() -> str:

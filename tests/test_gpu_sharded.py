@@ -1,0 +1,122 @@
+"""Sharded paths on one GPU.
+
+Neuron sharding: P ranks are emulated as P handles on the same device, each
+running its own cooperative training launch on its own thread, exchanging
+the per-step winner through each other's mailboxes (the same kernel path a
+multi-GPU run takes over NVLink, with same-device pointers instead of IPC
+mappings).  Bar: BMU log identical and weights bit-identical to P = 1 (and
+to the oracle's BMU log).  Document sharding: per-document outputs of the
+shards equal the unsharded call."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import bank_corpus, init_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def som():
+    from paper_1905_09598_b200 import som as s
+    s.lib()
+    return s
+
+
+def _run_sharded(som, P, rows, cols, topo, X, W0, epochs, sigma0, seed, grid, t_ranges):
+    from paper_1905_09598_b200.dist import ShardedSOM
+    n, d = X.shape
+    # same-process ranks: mailboxes are exchanged as device pointers
+    ranks = [ShardedSOM(rows, cols, d, topo, r, P, device=0, defer_peers=True) for r in range(P)]
+    boxes = [s.mailbox_ptr() for s in ranks]
+    for s in ranks:
+        s.set_peers(boxes)
+        som.som_set_train_grid(s.h, grid)
+        s.set_weights(W0)
+    logs = [[] for _ in range(P)]
+    errors = []
+    bar = threading.Barrier(P)
+
+    def work(r):
+        try:
+            for (tb, te) in t_ranges:
+                log = np.empty(te - tb, np.int32)
+                bar.wait()
+                som.som_train_online(ranks[r].h, X, n, epochs, 0.1, sigma0, None, seed, tb, te, log)
+                bar.wait()
+                logs[r].append(log)
+        except Exception as e:   # surface in the main thread
+            errors.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    W = np.zeros((rows * cols, d), np.float32)
+    for s in ranks:
+        som.som_get_weights(s.h, W)          # each writes its own rows
+        som.som_destroy(s.h)
+    return W, [np.concatenate(l) for l in logs]
+
+
+@pytest.mark.parametrize("P,grid", [(1, 16), (2, 16), (4, 8)])
+def test_neuron_sharded_training_equals_unsharded(som, P, grid):
+    C = bank_corpus(300, 512, seed=41)
+    X = C.dense()
+    W0 = init_rows(X, 12 * 12, 41)
+    T = 4 * 300
+    W, logs = _run_sharded(som, P, 12, 12, 1, X, W0, 4, 6.0, 5, grid, [(0, 700), (700, T)])
+    with som.SOM(12, 12, 512, 1) as m:
+        m.set_weights(W0)
+        ref_log = np.empty(T, np.int32)
+        m.train_online(X, epochs=4, alpha0=0.1, sigma0=6.0, seed=5, bmu_log=ref_log)
+        Wref = m.get_weights()
+    for r in range(P):
+        assert np.array_equal(logs[r], ref_log), f"rank {r} BMU log differs"
+    assert np.array_equal(W, Wref)
+    Wo, logo = oracle.train_online(W0, 12, 12, 1, X, 4, 0.1, 6.0, 5)
+    assert np.array_equal(ref_log, logo)
+    assert np.abs(W - Wo).max() <= 1e-4
+
+
+def test_neuron_sharded_global_w_kernel(som):
+    """Shards that do not fit registers take the smem/global kernel."""
+    C = bank_corpus(200, 2002, seed=42)           # d % 4 != 0 -> train.cu
+    X = C.dense()
+    W0 = init_rows(X, 60, 42)
+    W, logs = _run_sharded(som, 2, 6, 10, 0, X, W0, 2, 5.0, 9, 16, [(0, 400)])
+    Wo, logo = oracle.train_online(W0, 6, 10, 0, X, 2, 0.1, 5.0, 9)
+    assert np.array_equal(logs[0], logo) and np.array_equal(logs[1], logo)
+    assert np.abs(W - Wo).max() <= 1e-4
+
+
+def test_sharded_handle_refuses_mapping(som):
+    with som.SOM(4, 4, 32, 1) as m:
+        som.som_comm_init(m.h, 0, 2)
+        assert som.som_comm_local_units(m.h) == 8
+        with pytest.raises(som.SomError) as e:
+            m.map(np.zeros((3, 32), np.float32))
+        assert e.value.status == som.SOM_EUNSUPPORTED
+
+
+def test_doc_sharded_mapping_equals_unsharded(som):
+    from paper_1905_09598_b200.dist import shard_range
+    C = bank_corpus(2001, 1500, seed=43)
+    X = C.dense()
+    W = init_rows(X, 100, 43)
+    with som.SOM(10, 10, 1500, 1) as m:
+        m.set_weights(W)
+        b1, b2, d1 = m.map(X)
+        parts = []
+        for r in range(3):
+            lo, hi = shard_range(X.shape[0], r, 3)
+            parts.append(m.map(np.ascontiguousarray(X[lo:hi])))
+            qe_r, te_r = m.errors(np.ascontiguousarray(X[lo:hi]))
+    assert np.array_equal(np.concatenate([p[0] for p in parts]), b1)
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), b2)
+    assert np.array_equal(np.concatenate([p[2] for p in parts]), d1)
