@@ -34,17 +34,21 @@ som_status fail(som_status st, const char* fmt, ...) {
     return st;
 }
 
+// Grow-only device scratch from the stream-ordered allocator: no
+// device-wide synchronisation (a plain cudaMalloc would wait for every
+// running kernel, e.g. another rank's persistent grid on the same device).
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
-    cudaError_t ensure(size_t bytes) {
+    cudaStream_t owner = nullptr;
+    cudaError_t ensure(size_t bytes, cudaStream_t st) {
         if (bytes <= cap) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         cap = 0;
         size_t want = std::max(bytes, (size_t)256);
-        cudaError_t e = cudaMalloc(&p, want);
-        if (e == cudaSuccess) cap = want;
+        cudaError_t e = cudaMallocAsync(&p, want, st);
+        if (e == cudaSuccess) { cap = want; owner = st; }
         return e;
     }
     void release() {
@@ -139,7 +143,7 @@ som_status stage_in(som_ctx* h, DevBuf& buf, const void* src, size_t bytes, cons
         *dev = src;
         return SOM_OK;
     }
-    CK(buf.ensure(bytes));
+    CK(buf.ensure(bytes, h->stream));
     CK(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, h->stream));
     *dev = buf.p;
     return SOM_OK;
@@ -174,7 +178,7 @@ som_status ensure_decay_table(som_ctx* h, int64_t T, int kind, double k, int64_t
         th.emplace_back(fill_decay, host.data() + (a - t0), a, b, T, kind, k);
     }
     for (auto& x : th) x.join();
-    CK(h->ftab.ensure(sizeof(double) * (size_t)std::max<int64_t>(cnt, 1)));
+    CK(h->ftab.ensure(sizeof(double) * (size_t)std::max<int64_t>(cnt, 1), h->stream));
     CK(cudaMemcpyAsync(h->ftab.p, host.data(), sizeof(double) * (size_t)cnt, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->f_T = T; h->f_kind = kind; h->f_k = k; h->f_t0 = t0; h->f_t1 = t1;
@@ -318,7 +322,7 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     const int NL = h->NL;
     const size_t rowb = sizeof(float) * (size_t)h->dim;
     if (is_device_ptr(X)) {
-        CK(h->keys.ensure(sizeof(int64_t) * (size_t)NL));
+        CK(h->keys.ensure(sizeof(int64_t) * (size_t)NL, h->stream));
         CK(cudaMemcpyAsync(h->keys.p, mine.data(), sizeof(int64_t) * (size_t)NL, cudaMemcpyHostToDevice, h->stream));
         CK(launch_gather_rows(X, (const int64_t*)h->keys.p, NL, h->dim, h->W, h->stream));
     } else {
@@ -419,14 +423,14 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
 
-    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.G + 64));
+    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.G + 64, h->stream));
     a.xchg = (unsigned long long*)h->xchg.p;
     a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.G);
     CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.G + 64, h->stream));
 
     const int64_t steps = t_end - t_begin;
     bool log_dev = bmu_log && is_device_ptr(bmu_log);
-    if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps));
+    if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps, h->stream));
     a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
 
     CK(cudaEventRecord(h->ev0, h->stream));
@@ -439,7 +443,8 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     unsigned abort_flag = 0;
-    CK(cudaMemcpy(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     if (abort_flag) {
         h->poisoned = true;
         return fail(SOM_ECUDA, "training exchange timed out (a CTA or rank stopped publishing its BMU candidate)");
@@ -477,6 +482,12 @@ som_status som_comm_init(som_ctx* h, int32_t rank, int32_t world) {
     // one 2 MiB-aligned allocation of its own so its IPC handle maps nothing else
     CK(cudaMalloc(&h->mail, 2u << 20));
     CK(cudaMemsetAsync(h->mail, 0, 2u << 20, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    // pre-size the per-call training scratch: ranks that share one device
+    // (tests) must not grow the memory pool while a peer grid is spinning
+    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * 1024 + 64, h->stream));
+    CK(h->ftab.ensure(sizeof(double) * ((size_t)1 << 20), h->stream));
+    CK(h->log.ensure(sizeof(int32_t) * ((size_t)1 << 20), h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->rank = rank;
     h->world = world;
@@ -587,7 +598,7 @@ som_status ensure_w_split(som_ctx* h, const float** whi, const float** wlo, cons
     const int dp = tc_padded_dim(h->dim);
     const size_t plane = sizeof(float) * (size_t)h->N * dp;
     if (!h->w_split_valid) {
-        CK(h->wsplit.ensure(2 * plane + sizeof(float) * (size_t)h->N));
+        CK(h->wsplit.ensure(2 * plane + sizeof(float) * (size_t)h->N, h->stream));
         char* base = (char*)h->wsplit.p;
         CK(launch_split_rows(h->W, h->N, h->dim, (float*)base, (float*)(base + plane), (float*)(base + 2 * plane),
                              h->stream));
@@ -612,10 +623,10 @@ som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, int32_t* b1
     // split-X chunk: up to 8 GiB of hi/lo planes (large chunks keep B panels hot)
     const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, ((int64_t)8 << 30) / (8 * (int64_t)dp)));
     const size_t plane = sizeof(float) * (size_t)chunk * dp;
-    CK(h->xsplit.ensure(2 * plane + sizeof(float) * (size_t)chunk));
+    CK(h->xsplit.ensure(2 * plane + sizeof(float) * (size_t)chunk, h->stream));
     char* xb = (char*)h->xsplit.p;
     const int tiles_n = tc_unit_tiles(h->N);
-    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles_n * (size_t)chunk));
+    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles_n * (size_t)chunk, h->stream));
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t m = std::min(chunk, n - r0);
         CK(fill(r0, m, (float*)xb, (float*)(xb + plane), (float*)(xb + 2 * plane)));
@@ -639,7 +650,7 @@ som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, in
     const int tiles_m = map_exact_tiles_m(n);
     const int tiles_n = map_exact_tiles_n(h->N);
     int nsplit = std::max(1, std::min(tiles_n, (2 * h->sm_count + tiles_m - 1) / tiles_m));
-    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)nsplit * (size_t)n));
+    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)nsplit * (size_t)n, h->stream));
     MapArgs a{h->W, h->N, Xd, n, h->dim, nsplit, (unsigned long long*)h->keys.p};
     CK(launch_map_exact(a, h->stream));
     CK(launch_map_merge(a.keys, nsplit, n, b1, b2, d2, h->stream));
@@ -657,7 +668,7 @@ som_status stage_outputs(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, fl
     o.host2 = bmu2 && !is_device_ptr(bmu2);
     o.host3 = d2 && !is_device_ptr(d2);
     const size_t per = sizeof(int32_t) * 2 + sizeof(float);
-    CK(h->outs.ensure(per * (size_t)std::max<int64_t>(n, 1)));
+    CK(h->outs.ensure(per * (size_t)std::max<int64_t>(n, 1), h->stream));
     char* base = (char*)h->outs.p;
     o.b1 = (bmu1 && !o.host1) ? bmu1 : (int32_t*)base;
     o.b2 = (bmu2 && !o.host2) ? bmu2 : ((bmu2 || need_all) ? (int32_t*)(base + sizeof(int32_t) * (size_t)n) : nullptr);
@@ -737,7 +748,7 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
     }
     // densify in chunks of <= 1 GiB and map each chunk
     const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));
-    CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim));
+    CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim, h->stream));
     int launches = 0;
     CK(cudaEventRecord(h->ev0, h->stream));
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
@@ -773,7 +784,7 @@ som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double*
     CK(cudaEventRecord(h->ev0, h->stream));
     if ((st = map_dense_dev(h, (const float*)Xd, n, o.b1, o.b2, o.d2, &launches))) return st;
     const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
-    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2)));
+    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2), h->stream));
     double* partial = (double*)h->red.p;
     unsigned long long* pcnt = (unsigned long long*)(partial + nb);
     double* osum = (double*)(pcnt + nb);
@@ -812,7 +823,7 @@ som_status som_umatrix(som_ctx* h, float* U) {
     const bool dev = is_device_ptr(U);
     float* Ud = U;
     if (!dev) {
-        CK(h->outs.ensure(sizeof(float) * (size_t)h->N));
+        CK(h->outs.ensure(sizeof(float) * (size_t)h->N, h->stream));
         Ud = (float*)h->outs.p;
     }
     CK(cudaEventRecord(h->ev0, h->stream));

@@ -113,6 +113,23 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
     }
 }
 
+// Launch a persistent training grid.  Single rank: cooperative launch (the
+// driver guarantees all G CTAs are co-resident).  Neuron-sharded: a plain
+// launch after checking that G CTAs fit at once (one per SM), so that ranks
+// emulated on one device (tests) can run their grids concurrently; each
+// rank of a real multi-GPU run owns its device.
+inline cudaError_t launch_persistent(const void* fn, const TrainArgs& a, int threads, size_t smem, void** params,
+                                     cudaStream_t st) {
+    if (a.world <= 1) return cudaLaunchCooperativeKernel(fn, dim3(a.G), dim3(threads), params, smem, st);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (a.G > sms * per_sm) return cudaErrorCooperativeLaunchTooLarge;
+    return cudaLaunchKernel(fn, dim3(a.G), dim3(threads), params, smem, st);
+}
+
 // global unit index of local unit l
 __device__ __forceinline__ int global_unit(const TrainArgs& a, int l) { return a.rank + a.world * l; }
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -277,8 +277,7 @@ cudaError_t launch_train(const TrainArgs& a, size_t smem, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     TrainArgs args = a;
     void* params[] = {&args};
-    return cudaLaunchCooperativeKernel((const void*)som_train_kernel, dim3(a.G), dim3(kTrainThreads), params,
-                                       smem, st);
+    return launch_persistent((const void*)som_train_kernel, a, kTrainThreads, smem, params, st);
 }
 
 }  // namespace som

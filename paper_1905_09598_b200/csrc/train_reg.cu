@@ -246,8 +246,7 @@ cudaError_t launch_one(const TrainArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     TrainArgs args = a;
     void* params[] = {&args};
-    return cudaLaunchCooperativeKernel((const void*)som_train_reg_kernel<SMAX, KJ>, dim3(a.G), dim3(NT), params,
-                                       smem, st);
+    return launch_persistent((const void*)som_train_reg_kernel<SMAX, KJ>, a, NT, smem, params, st);
 }
 
 int smax_of(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 99; }

@@ -26,8 +26,13 @@ def som():
 
 
 def _run_sharded(som, P, rows, cols, topo, X, W0, epochs, sigma0, seed, grid, t_ranges):
+    import torch
+
     from paper_1905_09598_b200.dist import ShardedSOM
     n, d = X.shape
+    # device-resident inputs/outputs: ranks sharing one device must not
+    # allocate while a peer's grid spins
+    Xd = torch.from_numpy(X).cuda()
     # same-process ranks: mailboxes are exchanged as device pointers
     ranks = [ShardedSOM(rows, cols, d, topo, r, P, device=0, defer_peers=True) for r in range(P)]
     boxes = [s.mailbox_ptr() for s in ranks]
@@ -42,11 +47,11 @@ def _run_sharded(som, P, rows, cols, topo, X, W0, epochs, sigma0, seed, grid, t_
     def work(r):
         try:
             for (tb, te) in t_ranges:
-                log = np.empty(te - tb, np.int32)
+                log = torch.empty(te - tb, dtype=torch.int32, device="cuda")
                 bar.wait()
-                som.som_train_online(ranks[r].h, X, n, epochs, 0.1, sigma0, None, seed, tb, te, log)
+                som.som_train_online(ranks[r].h, Xd, n, epochs, 0.1, sigma0, None, seed, tb, te, log)
                 bar.wait()
-                logs[r].append(log)
+                logs[r].append(log.cpu().numpy())
         except Exception as e:   # surface in the main thread
             errors.append(e)
             bar.abort()
@@ -60,7 +65,7 @@ def _run_sharded(som, P, rows, cols, topo, X, W0, epochs, sigma0, seed, grid, t_
     W = np.zeros((rows * cols, d), np.float32)
     for s in ranks:
         som.som_get_weights(s.h, W)          # each writes its own rows
-        som.som_destroy(s.h)
+        s.close()
     return W, [np.concatenate(l) for l in logs]
 
 
