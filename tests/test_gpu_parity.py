@@ -245,3 +245,18 @@ def test_c2_kernel_variants_agree(som):
     assert c1[1] == 2
     for mode in (som.SOM_TRAIN_W_SHARED, som.SOM_TRAIN_W_GLOBAL):
         assert np.array_equal(out[mode][1], l1) and np.array_equal(out[mode][0], W1)
+
+
+@pytest.mark.slow
+def test_c2_full_schedule(som):
+    """c2 in full: 20x20 hex, 5000 x 3000, 100 epochs = 500,000 steps
+    (BASELINE.json configs[1]).  The oracle runs on all host cores (OpenMP
+    over units; each unit's sum stays sequential).  BMU sequence identical
+    over the whole schedule, weights within 1e-4."""
+    C = bank_corpus(5000, 3000, seed=1)
+    X = C.dense()
+    W0 = init_rows(X, 400, 1001)
+    W, log, Wo, logo = _train_both(som, 20, 20, 1, X, W0, 100, 0.1, 10.0, 1)
+    _assert_train(W, log, Wo, logo)
+    print(f" [c2 full: 500000 steps, BMU log identical, max|dW| = {np.abs(W - Wo).max():.3g}, "
+          f"bit-identical weights: {np.array_equal(W, Wo)}]", end="")

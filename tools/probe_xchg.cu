@@ -80,6 +80,73 @@ __global__ void p_gather_rep(unsigned long long* slots, int steps, int R, unsign
     if (threadIdx.x == 0 && acc == 42) out[0] = acc;
 }
 
+// P0b: reducer + broadcast: all CTAs publish; CTA 0 polls the G slots, writes
+// one tagged result word; the others poll only that word.  `sleep_ns` adds
+// a nanosleep backoff between polls of the all-gather variant when > 0.
+__global__ void p_reduce_bcast(unsigned long long* slots, unsigned long long* result, int steps,
+                               unsigned long long* out) {
+    const int G = gridDim.x, b = blockIdx.x, lane = threadIdx.x & 31;
+    unsigned long long acc = 0;
+    for (int t = 0; t < steps; ++t) {
+        if (threadIdx.x < 32) {
+            const unsigned long long tag = 0x80ull | (unsigned long long)(t & 0x7F);
+            unsigned long long* s = slots + (size_t)(t & 1) * G;
+            if (lane == 0) st_relaxed_u64(s + b, ((unsigned long long)((b * 7 + t) % 1000) << 8) | tag);
+            if (b == 0) {
+                unsigned long long m;
+                for (;;) {
+                    unsigned long long mm = ~0ull;
+                    bool ok = true;
+                    for (int j = lane; j < G; j += 32) {
+                        unsigned long long v = ld_relaxed_u64(s + j);
+                        ok &= (v & 0xFF) == tag;
+                        mm = umin(mm, v);
+                    }
+                    if (__all_sync(0xffffffffu, ok)) {
+                        for (int o = 16; o; o >>= 1) mm = umin(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+                        m = mm;
+                        break;
+                    }
+                }
+                if (lane == 0) st_relaxed_u64(result + (t & 1), m);
+                acc += m;
+            } else {
+                for (;;) {
+                    unsigned long long v = ld_relaxed_u64(result + (t & 1));
+                    if ((v & 0xFF) == tag) { acc += v; break; }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && acc == 42) out[0] = acc;
+}
+
+__global__ void p_gather_sleep(unsigned long long* slots, int steps, int sleep_ns, unsigned long long* out) {
+    const int G = gridDim.x, b = blockIdx.x, lane = threadIdx.x & 31;
+    unsigned long long acc = 0;
+    for (int t = 0; t < steps; ++t) {
+        if (threadIdx.x < 32) {
+            unsigned long long tag = 0x80ull | (unsigned long long)(t & 0x7F);
+            unsigned long long* s = slots + (size_t)(t & 1) * G;
+            if (lane == 0) st_relaxed_u64(s + b, ((unsigned long long)((b * 7 + t) % 1000) << 8) | tag);
+            for (;;) {
+                unsigned long long m = ~0ull;
+                bool ok = true;
+                for (int j = lane; j < G; j += 32) {
+                    unsigned long long v = ld_relaxed_u64(s + j);
+                    ok &= (v & 0xFF) == tag;
+                    m = umin(m, v);
+                }
+                if (__all_sync(0xffffffffu, ok)) { acc += m; break; }
+                __nanosleep(sleep_ns);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && acc == 42) out[0] = acc;
+}
+
 // P1: atomicMin into slot[t%3] + release-add arrival counter; poll counter (acquire), read slot
 __global__ void p_atomic(unsigned long long* slot3, unsigned* cnt3, int steps, unsigned long long* out) {
     const int G = gridDim.x, b = blockIdx.x;
@@ -175,6 +242,36 @@ int main() {
         CK(cudaEventElapsedTime(&ms, e0, e1));
         return ms * 1e3 / steps;
     };
+    if (getenv("PROBE_QUICK")) {
+        for (int G : {148, 128, 64, 32}) {
+            float us = timeit([&] {
+                CK(cudaMemset(slots, 0, 2 * 148 * 16 * 8));
+                int st = steps, sd = 1;
+                void* a[] = {&slots, &st, &sd, &out};
+                CK(cudaLaunchCooperativeKernel((void*)p_gather, G, 512, a, 0, 0));
+            });
+            printf("  \"gather_G%d\": %.3f,\n", G, us);
+            unsigned long long* res = slots + 2 * 148 * 8;
+            us = timeit([&] {
+                CK(cudaMemset(slots, 0, 2 * 148 * 16 * 8));
+                int st = steps;
+                void* a[] = {&slots, &res, &st, &out};
+                CK(cudaLaunchCooperativeKernel((void*)p_reduce_bcast, G, 512, a, 0, 0));
+            });
+            printf("  \"reduce_bcast_G%d\": %.3f,\n", G, us);
+            for (int sl : {20, 50, 100}) {
+                us = timeit([&] {
+                    CK(cudaMemset(slots, 0, 2 * 148 * 16 * 8));
+                    int st = steps, s2 = sl;
+                    void* a[] = {&slots, &st, &s2, &out};
+                    CK(cudaLaunchCooperativeKernel((void*)p_gather_sleep, G, 512, a, 0, 0));
+                });
+                printf("  \"gather_sleep%d_G%d\": %.3f,\n", sl, G, us);
+            }
+        }
+        printf("  \"steps\": %d\n}\n", steps);
+        return 0;
+    }
     for (int stride : {1, 16}) {
         for (int G : {148, 128, 96, 74, 64, 48, 32, 16}) {
             float us = timeit([&] {

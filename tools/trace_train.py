@@ -13,6 +13,7 @@ from synth import CONFIGS, bank_corpus, init_rows  # noqa: E402
 cfg = dict(CONFIGS[sys.argv[1]])
 grid = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3000
+tb = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 C = bank_corpus(cfg["n"], cfg["d"], seed=1)
 X = torch.from_numpy(C.dense()).cuda()
 W0 = torch.from_numpy(init_rows(C.dense(), cfg["rows"] * cfg["cols"], 1001)).cuda()
@@ -21,12 +22,12 @@ som.som_set_train_grid(m.h, grid)
 tr = torch.zeros(148 * steps * 8, dtype=torch.int64, device="cuda")
 som.som_set_trace(m.h, tr, steps)
 m.set_weights(W0)
-som.som_train_online(m.h, X, cfg["n"], cfg["epochs"], 0.1, cfg["sigma0"], None, 1, 0, steps, None)
+som.som_train_online(m.h, X, cfg["n"], cfg["epochs"], 0.1, cfg["sigma0"], None, 1, tb, tb + steps, None)
 ms, units, _ = som.som_last_stats(m.h)
 G, k = som.som_last_train_config(m.h)
 t = tr.view(148, steps, 8)[:G].cpu().numpy().astype(np.float64)[:, 200:]
 names = ["fused+reduce", "issue_x+barA", "w0 key", "publish+poll", "h compute", "x shift/read", "barB"]
-print(f"{sys.argv[1]} G={G} kernel={k}: {1000 * ms / units:.3f} us/step (event)")
+print(f"{sys.argv[1]} t=[{tb},{tb + steps}) G={G} kernel={k}: {1000 * ms / units:.3f} us/step (event)")
 d = np.diff(t, axis=2)                        # [G][steps][7]
 for i in range(7):
     med = np.median(d[:, :, i], axis=1)       # per CTA
