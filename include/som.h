@@ -133,7 +133,8 @@ som_status som_set_train_mode(som_ctx *h, int32_t mode);
 som_status som_set_train_grid(som_ctx *h, int32_t grid);
 
 /* Grid and kernel variant of the last som_train_online call:
- * kernel 0 = W in global memory, 1 = W in shared memory, 2 = W in registers. */
+ * kernel 0 = W in global memory (generic), 1 = W in shared memory,
+ * 2 = W in registers, 3 = W in global memory (pipelined, d % 4 == 0). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* ---- Neuron sharding: online training of one map across

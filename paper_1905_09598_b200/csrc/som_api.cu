@@ -419,7 +419,11 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
         return fail(SOM_EUNSUPPORTED, "W slice (%zu B/CTA) does not fit shared memory", smem);
     if (h->train_mode == SOM_TRAIN_W_GLOBAL) a.w_smem = 0;
     if (!a.w_smem) smem = train_smem_bytes(a.S, a.dimp, 0);
+    // maps that do not fit on chip stream from global memory with the
+    // pipelined kernel (train_glb.cu) when its layout applies
+    const bool use_glb = !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
     if (use_reg) smem = sizeof(float) * 3 * (size_t)a.dimp;
+    if (use_glb) smem = sizeof(float) * 2 * (size_t)a.dimp;
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
 
@@ -435,10 +439,11 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
 
     CK(cudaEventRecord(h->ev0, h->stream));
     if (use_reg) CK(launch_train_reg(a, h->stream));
+    else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
     h->last_grid = a.G;
-    h->last_kernel = use_reg ? 2 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_reg ? 2 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

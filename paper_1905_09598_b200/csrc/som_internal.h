@@ -144,6 +144,9 @@ cudaError_t launch_train(const TrainArgs& a, size_t smem, cudaStream_t st);
 // per-CTA share of W (S units x ceil(d/2048) float4 chunks per thread).
 bool train_reg_supported(int S, int dim);
 cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st);
+// pipelined global-memory variant (train_glb.cu) for maps that do not fit on chip
+bool train_glb_supported(int S, int dim);
+cudaError_t launch_train_glb(const TrainArgs& a, cudaStream_t st);
 
 // Exact (fp64-accumulated) batch mapping: partial top-2 keys per doc per
 // neuron split, then merged.  keys: [nsplit][n][2] u64 scratch.

@@ -260,3 +260,19 @@ def test_c2_full_schedule(som):
     _assert_train(W, log, Wo, logo)
     print(f" [c2 full: 500000 steps, BMU log identical, max|dW| = {np.abs(W - Wo).max():.3g}, "
           f"bit-identical weights: {np.array_equal(W, Wo)}]", end="")
+
+
+def test_c3_prefix_global_kernel(som):
+    """c3 shape (50x50 hex, 10k terms; W = 100 MB streams from L2/HBM): the
+    pipelined global-memory kernel, first 150 steps, against the oracle."""
+    C = bank_corpus(3000, 10000, seed=3)
+    X = C.dense()
+    W0 = init_rows(X, 2500, 1003)
+    with som.SOM(50, 50, 10000, 1) as m:
+        m.set_weights(W0)
+        log = np.empty(150, np.int32)
+        m.train_online(X, epochs=10, alpha0=0.1, sigma0=25.0, seed=3, t_end=150, bmu_log=log)
+        assert som.som_last_train_config(m.h)[1] == 3
+        W = m.get_weights()
+    Wo, logo = oracle.train_online(W0, 50, 50, 1, X, 10, 0.1, 25.0, 3, t_end=150)
+    _assert_train(W, log, Wo, logo)
