@@ -422,7 +422,7 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     // maps that do not fit on chip stream from global memory with the
     // pipelined kernel (train_glb.cu) when its layout applies
     const bool use_glb = !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
-    if (use_reg) smem = sizeof(float) * 3 * (size_t)a.dimp;
+    if (use_reg) smem = sizeof(float) * (3 * (size_t)a.dimp + (size_t)a.rows * (a.topo == 0 ? a.cols : 2 * a.cols));
     if (use_glb) smem = sizeof(float) * 2 * (size_t)a.dimp;
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);

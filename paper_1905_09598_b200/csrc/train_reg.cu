@@ -36,13 +36,38 @@ __device__ __forceinline__ float4 eq1u(float h, float4 w, float4 x) {
     return w;
 }
 
+// Warp sum of SMAX per-lane values with a multi-value butterfly: at each of
+// the first log2(SMAX) levels a lane keeps half of its slots and sends the
+// other half, so the warp issues 2*(SMAX-1) + 2*(5 - log2 SMAX) shuffles
+// instead of 10*SMAX.  Returns the full warp sum of slot `*slot` in lanes
+// whose low (5 - log2 SMAX) bits are zero.
+template <int SMAX>
+__device__ __forceinline__ double butterfly_sum(double (&v)[SMAX], int lane, int* slot) {
+    int sl = 0;
+#pragma unroll
+    for (int width = SMAX, off = 16; width > 1; width >>= 1, off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < width / 2; ++i) {
+            const double send = upper ? v[i] : v[i + width / 2];
+            const double keep = upper ? v[i + width / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+        sl = sl * 2 + (upper ? 1 : 0);
+    }
+    double x = v[0];
+#pragma unroll
+    for (int off = 16 / SMAX; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    *slot = sl;
+    return x;
+}
+
 template <int SMAX, int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a) {
     __shared__ double part[NW][SMAX];        // per-warp partial distance of each unit
-    __shared__ float hs[SMAX];
-    __shared__ int upd[SMAX];
+    __shared__ int s_c;                      // winner of the current step
     __shared__ int s_abort;
-    extern __shared__ __align__(16) float xring[];   // [3][dimp]
+    extern __shared__ __align__(16) float xring[];   // [3][dimp] x ring, then the h table
 
     const int b = blockIdx.x, G = a.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -50,6 +75,11 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     const int d4 = a.dimp >> 2;
     const float4* W4 = reinterpret_cast<const float4*>(a.W);
     float4* ring4 = reinterpret_cast<float4*>(xring);
+    // neighbourhood table of the step: h for every lattice offset
+    // (|di|, |dj| rect or |2 dx| hex), -1 outside the cutoff (R4, R5)
+    const int W2 = a.topo == 0 ? a.cols : 2 * a.cols;
+    const int HT = a.rows * W2;
+    float* htab = xring + 3 * (size_t)a.dimp;
 
     bool valid[KJ];
 #pragma unroll
@@ -58,28 +88,27 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     float4 w[SMAX][KJ];
     float4 xp[KJ], xc[KJ];
     double xd[KJ][4];
+    float hh[SMAX];          // pending update of each unit (h, or < 0: none)
+    int ui[SMAX], uj[SMAX];  // lattice coordinates of this CTA's units
 #pragma unroll
-    for (int s = 0; s < SMAX; ++s)
+    for (int s = 0; s < SMAX; ++s) {
 #pragma unroll
         for (int j = 0; j < KJ; ++j) {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s < Sb && valid[j]) v = W4[(int64_t)(b + s * G) * d4 + threadIdx.x + j * NT];
             w[s][j] = v;
         }
+        hh[s] = -1.0f;
+        const int u = global_unit(a, b + s * G);
+        ui[s] = u / a.cols;
+        uj[s] = u - ui[s] * a.cols;
+    }
 #pragma unroll
     for (int j = 0; j < KJ; ++j) {
         xp[j] = xc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         xd[j][0] = xd[j][1] = xd[j][2] = xd[j][3] = 0.0;
     }
-    if (threadIdx.x < SMAX) { hs[threadIdx.x] = 0.0f; upd[threadIdx.x] = 0; }
     if (threadIdx.x == 0) s_abort = 0;
-    // lattice coordinates of unit s = lane (warp 0, lanes < Sb)
-    int my_i = 0, my_j = 0;
-    if (lane < SMAX && lane < Sb) {
-        const int u = global_unit(a, b + lane * G);
-        my_i = u / a.cols;
-        my_j = u - my_i * a.cols;
-    }
 
     auto issue_x = [&](int64_t t) {
         if (t < a.t1) {
@@ -111,14 +140,12 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     shift_x(a.t0);            // xc = x_{t0}, xd = fp64(x_{t0})
     __syncthreads();
 
-    double f_cur = 0.0;
     for (int64_t t = a.t0; t < a.t1; ++t) {
         unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
         if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
 #define TRACE(p) do { if (tr) tr[p] = globaltimer_ns(); } while (0)
         TRACE(0);
-        if (warp == 0) f_cur = a.f_tab[t - a.t0];   // consumed after the exchange
 
         // ---- fused pass on registers: pending update (t-1), then D_u(x_t)
         double acc[SMAX];
@@ -126,8 +153,8 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         for (int s = 0; s < SMAX; ++s) {
             acc[s] = 0.0;
             if (s < Sb) {
-                const float h = hs[s];
-                const bool up = upd[s] != 0;
+                const float h = hh[s];
+                const bool up = h >= 0.0f;
                 double a0 = 0.0, a1 = 0.0;
 #pragma unroll
                 for (int j = 0; j < KJ; ++j) {
@@ -147,13 +174,10 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
                 acc[s] = a0 + a1;
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int s = 0; s < SMAX; ++s) acc[s] += __shfl_xor_sync(0xffffffffu, acc[s], o);
-        if (lane == 0) {
-#pragma unroll
-            for (int s = 0; s < SMAX; ++s) part[warp][s] = acc[s];
+        {
+            int slot;
+            const double v = butterfly_sum<SMAX>(acc, lane, &slot);
+            if ((lane & (32 / SMAX - 1)) == 0) part[warp][slot] = v;
         }
         TRACE(1);
         issue_x(t + 2);
@@ -178,49 +202,55 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
             shift_x(t + 1);                       // hidden behind the poll
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
-            if (stop && lane == 0) s_abort = 1;
             const int c = key_unit(gmin);
             TRACE(4);
-            if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
-            if (lane < SMAX && lane < Sb) {
-                // schedule (R1-R3) and neighbourhood of step t (R4, R5)
-                const double alpha = a.alpha0 * f_cur;
-                double sigma = a.sigma0 * f_cur;
-                if (sigma < a.sigma_min) sigma = a.sigma_min;
-                const double two_s2 = 2.0 * sigma * sigma;
-                const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
-                const int ic = c / a.cols, jc = c - ic * a.cols;
-                const double di = (double)(my_i - ic);
-                double g2;
-                if (a.topo == 0) {
-                    const double dj = (double)(my_j - jc);
-                    g2 = di * di + dj * dj;
-                } else {
-                    const double dx2 = (double)(2 * (my_j - jc) + ((my_i & 1) - (ic & 1)));
-                    g2 = 0.25 * (dx2 * dx2) + 0.75 * (di * di);
-                }
-                const bool up = g2 <= r2;
-                upd[lane] = up ? 1 : 0;
-                hs[lane] = up ? (float)(alpha * exp(-g2 / two_s2)) : 0.0f;
+            if (lane == 0) {
+                s_c = c;
+                if (stop) s_abort = 1;
+                if (b == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
             }
-            __syncwarp();
             TRACE(5);
         } else {
             shift_x(t + 1);
+            // neighbourhood table of step t (schedule R1-R3, kernel R4, cutoff
+            // R5), built while warp 0 waits on the exchange
+            const double f = a.f_tab[t - a.t0];
+            const double alpha = a.alpha0 * f;
+            double sigma = a.sigma0 * f;
+            if (sigma < a.sigma_min) sigma = a.sigma_min;
+            const double two_s2 = 2.0 * sigma * sigma;
+            const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
+            for (int e = threadIdx.x - 32; e < HT; e += NT - 32) {
+                const int di = e / W2, dx = e - di * W2;
+                const double ddi = (double)di, ddx = (double)dx;
+                const double g2 = a.topo == 0 ? ddi * ddi + ddx * ddx : 0.25 * (ddx * ddx) + 0.75 * (ddi * ddi);
+                htab[e] = g2 <= r2 ? (float)(alpha * exp(-g2 / two_s2)) : -1.0f;
+            }
         }
         TRACE(6);
-        __syncthreads();   // B: winner's neighbourhood ready
+        __syncthreads();   // B: winner and neighbourhood table ready
         TRACE(7);
 #undef TRACE
         if (s_abort) break;
+        {
+            // every thread looks up h for its CTA's units (exact g2 offsets)
+            const int c = s_c;
+            const int ic = c / a.cols, jc = c - ic * a.cols;
+#pragma unroll
+            for (int s = 0; s < SMAX; ++s) {
+                const int di = abs(ui[s] - ic);
+                const int dx = a.topo == 0 ? abs(uj[s] - jc) : abs(2 * (uj[s] - jc) + ((ui[s] & 1) - (ic & 1)));
+                hh[s] = s < Sb ? htab[di * W2 + dx] : -1.0f;
+            }
+        }
     }
 
     if (a.t1 > a.t0 && !s_abort) {
         // flush the update of the last step (x_{t1-1} is in xp)
 #pragma unroll
         for (int s = 0; s < SMAX; ++s) {
-            if (s < Sb && upd[s]) {
-                const float h = hs[s];
+            if (s < Sb && hh[s] >= 0.0f) {
+                const float h = hh[s];
 #pragma unroll
                 for (int j = 0; j < KJ; ++j)
                     if (valid[j]) w[s][j] = eq1u(h, w[s][j], xp[j]);
@@ -238,9 +268,14 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     }
 }
 
+size_t reg_smem_bytes(const TrainArgs& a) {
+    const int W2 = a.topo == 0 ? a.cols : 2 * a.cols;
+    return sizeof(float) * (3 * (size_t)a.dimp + (size_t)a.rows * W2);
+}
+
 template <int SMAX, int KJ>
 cudaError_t launch_one(const TrainArgs& a, cudaStream_t st) {
-    const size_t smem = sizeof(float) * 3 * (size_t)a.dimp;
+    const size_t smem = reg_smem_bytes(a);
     cudaError_t e = cudaFuncSetAttribute(som_train_reg_kernel<SMAX, KJ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
