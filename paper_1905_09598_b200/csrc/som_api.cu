@@ -437,11 +437,42 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps, h->stream));
     a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
 
+    // W streamed from global memory every step: keep it resident in L2 with a
+    // persisting access-policy window (random X rows stream past it), undone
+    // after the launch so the caller's stream is left as it was.
+    bool l2_window = false;
+    if (!use_reg && !a.w_smem) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+        const size_t wbytes = sizeof(float) * (size_t)h->NL * h->dim;
+        if (max_persist > 0 && max_window > 0) {
+            const size_t win = std::min(wbytes, (size_t)max_window);
+            const size_t keep = std::min(win, (size_t)max_persist);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep) == cudaSuccess) {
+                cudaStreamAttrValue at{};
+                at.accessPolicyWindow.base_ptr = h->W;
+                at.accessPolicyWindow.num_bytes = win;
+                at.accessPolicyWindow.hitRatio = (float)((double)keep / (double)win);
+                at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                l2_window = cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at) == cudaSuccess;
+            }
+            cudaGetLastError();
+        }
+    }
     CK(cudaEventRecord(h->ev0, h->stream));
     if (use_reg) CK(launch_train_reg(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
+    if (l2_window) {
+        cudaStreamAttrValue at{};
+        at.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at);
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
     h->last_grid = a.G;
     h->last_kernel = use_reg ? 2 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)

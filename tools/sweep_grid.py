@@ -22,7 +22,7 @@ for mode in modes:
         som.som_set_train_mode(m.h, mode)
         som.som_set_train_grid(m.h, G)
         print(f"-- mode {mode} grid {G}", flush=True)
-        best = 1e30
+        best, units = 1e30, 0
         for rep in range(2):
             m.set_weights(W0)
             try:
@@ -32,6 +32,8 @@ for mode in modes:
                 break
             ms, units, _ = som.som_last_stats(m.h)
             best = min(best, ms)
+        if units == 0:
+            continue
         g, k = som.som_last_train_config(m.h)
         Wn = torch.empty_like(W0)
         som.som_get_weights(m.h, Wn)
