@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--map-docs", type=int, default=200000, help="documents in the c5-shaped mapping leg (0 = skip)")
+    p.add_argument("--c3-steps", type=int, default=20000, help="steps of the c3 training leg (0 = skip)")
     return p.parse_args()
 
 
@@ -175,6 +176,60 @@ def mapping_leg(som, torch, args, local, seed):
                          "peak_source": src,
                          "work": "3 x 2*n*N*d executed TF32 flop per call (3xTF32 split), incl. CSR split + merge",
                          "algorithmic_fp32_tflops": flop / (ms / 1000.0) / 1e12}}
+
+
+def updated_units(rows, cols, topo, bmu_log, t0, T, sigma0, eps=1e-4, k=math.log(100.0), sigma_min=1.0):
+    """H_t: units inside the cutoff radius of each step's winner (R5), from the
+    BMU log and the schedule (host-side bookkeeping for the byte count)."""
+    ii, jj = np.divmod(np.arange(rows * cols), cols)
+    out = np.empty(len(bmu_log), np.int64)
+    for s, c in enumerate(bmu_log):
+        tau = (t0 + s) / T
+        sig = max(sigma_min, sigma0 * math.exp(-k * tau * tau))
+        r2 = 2.0 * sig * sig * math.log(1.0 / eps)
+        ic, jc = divmod(int(c), cols)
+        di = (ii - ic).astype(np.float64)
+        if topo == 0:
+            g2 = di * di + (jj - jc) ** 2
+        else:
+            dx2 = (2 * (jj - jc) + ((ii & 1) - (ic & 1))).astype(np.float64)
+            g2 = 0.25 * dx2 * dx2 + 0.75 * di * di
+        out[s] = int(np.count_nonzero(g2 <= r2))
+    return out
+
+
+def train_c3_leg(som, torch, args, local, seed):
+    """Online training in the bandwidth-bound regime: c3 (50x50 hex, 50k x 10k,
+    W = 100 MB streamed through L2/HBM every step), first `--c3-steps` steps."""
+    cfg = CONFIGS["c3"]
+    n, d, N = cfg["n"], cfg["d"], cfg["rows"] * cfg["cols"]
+    T = cfg["epochs"] * n
+    steps = args.c3_steps
+    C = bank_corpus(n, d, seed=seed + 300)
+    X = torch.from_numpy(C.dense()).cuda()
+    mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+    som.som_set_stream(mm.h, torch.cuda.current_stream())
+    som.som_init_random(mm.h, X, n, seed + 1300)
+    log = torch.empty(steps, dtype=torch.int32, device="cuda")
+    som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, 2000, None)   # warm-up
+    som.som_init_random(mm.h, X, n, seed + 1300)
+    som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, steps, log)
+    ms, _, _ = som.som_last_stats(mm.h)
+    g, kern = som.som_last_train_config(mm.h)
+    H = updated_units(cfg["rows"], cfg["cols"], cfg["topo"], log.cpu().numpy(), 0, T, cfg["sigma0"])
+    algo = float(4.0 * N * d * steps + 4.0 * d * H.sum() + 4.0 * d * steps)   # read W, write updated rows, read x
+    gbps = algo / (ms / 1000.0) / 1e9
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        hbm = float(json.load(f)["hbm_gbs"])
+    mm.close()
+    return {"workload": f"c3: {cfg['rows']}x{cfg['cols']} hex, {n} x {d}, steps [0, {steps}) of T = {T}",
+            "samples_per_s": steps / (ms / 1000.0), "us_per_step": 1000.0 * ms / steps,
+            "mean_updated_units": float(H.mean()),
+            "roofline": {"bound": "hbm", "kernel": f"som_train_glb_kernel (kernel id {kern}), G={g}",
+                         "achieved": gbps, "peak": hbm, "unit": "GB/s", "frac": gbps / hbm,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+                         "work": "4*N*d read + 4*H_t*d written + 4*d per sample (H_t from the BMU log); "
+                                 "an L2 persisting window keeps part of W on chip, so frac can exceed 1"}}
 
 
 # ------------------------------------------------------------- oracle legs
@@ -330,6 +385,7 @@ def run_b200(args, rank, world, local):
     kname = {0: "som_train_kernel (W global)", 1: "som_train_kernel (W smem)",
              2: "som_train_reg_kernel (W registers)"}.get(k_used, "?")
     mapping = mapping_leg(som, torch, args, local, seed) if args.map_docs > 0 else None
+    train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -365,6 +421,7 @@ def run_b200(args, rank, world, local):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "mapping": mapping,
+        "train_c3": train_c3,
         "roofline": {"bound": "alu", "kernel": f"{kname}, G={g_used}", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
