@@ -14,6 +14,9 @@
 //    each prototype element costs one F2F.F64.F32 (the ~16/clk/SM pipe);
 //  * updated rows are written back with st.global.cg (L2).
 // Units are dealt cyclically (u = b + s*G); s runs over this CTA's units.
+#include <algorithm>
+#include <cstdlib>
+
 #include "som_device.cuh"
 #include "som_internal.h"
 
@@ -183,6 +186,200 @@ __global__ void __launch_bounds__(NT, 1) som_train_glb_kernel(const TrainArgs a)
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA row-ring variant (d <= 12288): thread 0 keeps R rows in flight with
+// cp.async.bulk (global -> shared, completion on one mbarrier per buffer),
+// continuing into the next step's first rows while the exchange runs, so
+// the loop is not exposed to L2/HBM latency row by row.  Rows are consumed
+// from shared memory; updated rows go back with st.global.cg.  Row q of the
+// CTA's sequence (q = step * Sb + s) lives in buffer q % R; the refill of
+// buffer q % R with row q + R is issued only after row q was processed and
+// written back (R <= Sb, so row q + R is final at that point).
+__device__ __forceinline__ void mbar_init_g(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITG_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITG_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"(sb) : "memory");
+}
+
+template <int KJ>
+__global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a, int R) {
+    __shared__ double part[kMaxSlotsG][NW];
+    __shared__ float hs[kMaxSlotsG];
+    __shared__ int upd[kMaxSlotsG];
+    __shared__ int s_abort;
+    __shared__ __align__(8) uint64_t mbar[8];
+    extern __shared__ __align__(128) float sm[];   // [dimp] x staging, then R rows of dimp
+
+    const int b = blockIdx.x, G = a.G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Sb = (a.N - b + G - 1) / G;
+    const int d4 = a.dimp >> 2;
+    const uint32_t row_bytes = (uint32_t)a.dim * 4u;
+    float4* W4 = reinterpret_cast<float4*>(a.W);
+    float4* xs4 = reinterpret_cast<float4*>(sm);
+    float4* rows4 = reinterpret_cast<float4*>(sm + a.dimp);
+    const int64_t nsteps = a.t1 - a.t0;
+    const int64_t total_rows = nsteps * Sb;
+
+    bool valid[KJ];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) valid[j] = threadIdx.x + j * NT < d4;
+
+    for (int s = threadIdx.x; s < kMaxSlotsG; s += NT) { hs[s] = 0.0f; upd[s] = 0; }
+    if (threadIdx.x == 0) {
+        s_abort = 0;
+        for (int r = 0; r < R; ++r) mbar_init_g(&mbar[r], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int64_t q = 0; q < R && q < total_rows; ++q)
+            bulk_row(rows4 + (size_t)q * d4, W4 + (int64_t)(b + (int)(q % Sb) * G) * d4, row_bytes, &mbar[q]);
+    }
+
+    auto stage = [&](int64_t t) {
+        if (t < a.t1) {
+            const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
+#pragma unroll
+            for (int j = 0; j < KJ; ++j)
+                if (valid[j]) cp_async16(xs4 + threadIdx.x + j * NT, src + threadIdx.x + j * NT);
+        }
+        cp_async_commit();
+    };
+    float4 xp[KJ], xc[KJ];
+    double xd[KJ][4];
+    stage(a.t0);
+    cp_async_wait_all();
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        xp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        xc[j] = valid[j] ? xs4[threadIdx.x + j * NT] : make_float4(0.f, 0.f, 0.f, 0.f);
+        xd[j][0] = xc[j].x; xd[j][1] = xc[j].y; xd[j][2] = xc[j].z; xd[j][3] = xc[j].w;
+    }
+    __syncthreads();
+
+    for (int64_t t = a.t0; t < a.t1; ++t) {
+        const int64_t qbase = (t - a.t0) * Sb;
+        for (int s = 0; s < Sb; ++s) {
+            const int64_t q = qbase + s;
+            const int buf = (int)(q % R);
+            mbar_wait_g(&mbar[buf], (uint32_t)((q / R) & 1));
+            const float4* rbuf = rows4 + (size_t)buf * d4;
+            const bool up = upd[s] != 0;
+            const float h = hs[s];
+            float4* row = W4 + (int64_t)(b + s * G) * d4;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < KJ; ++j) {
+                if (!valid[j]) continue;
+                const int c = threadIdx.x + j * NT;
+                float4 w = rbuf[c];
+                if (up) {
+                    w = eq1g(h, w, xp[j]);
+                    __stcg(row + c, w);
+                }
+                const double e0 = xd[j][0] - (double)w.x, e1 = xd[j][1] - (double)w.y;
+                const double e2 = xd[j][2] - (double)w.z, e3 = xd[j][3] - (double)w.w;
+                a0 = fma(e0, e0, a0);
+                a1 = fma(e1, e1, a1);
+                a0 = fma(e2, e2, a0);
+                a1 = fma(e3, e3, a1);
+            }
+            const double acc = warp_sum_f64(a0 + a1);
+            if (lane == 0) part[s][warp] = acc;
+            __syncthreads();   // buffer consumed, row written back
+            if (threadIdx.x == 0 && q + R < total_rows) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                const int rn = (int)((q + R) % Sb);
+                bulk_row(rows4 + (size_t)buf * d4, W4 + (int64_t)(b + rn * G) * d4, row_bytes, &mbar[buf]);
+            }
+        }
+
+        stage(t + 1);      // x_{t+1} into the staging buffer (consumed at the step start)
+
+        if (warp == 0) {
+            unsigned long long best = ~0ull;
+            for (int s = lane; s < Sb; s += 32) {
+                double tot = 0.0;
+#pragma unroll
+                for (int w8 = 0; w8 < NW; ++w8) tot += part[s][w8];
+                best = umin64(best, make_key((float)tot, global_unit(a, b + s * G)));
+            }
+            best = warp_min_u64(best);
+            xchg_publish(a, best, t, b, lane);
+            const double f = a.f_tab[t - a.t0];
+            int stop = 0;
+            const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
+            if (stop && lane == 0) s_abort = 1;
+            const int c = key_unit(gmin);
+            if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
+            const double alpha = a.alpha0 * f;
+            double sigma = a.sigma0 * f;
+            if (sigma < a.sigma_min) sigma = a.sigma_min;
+            const double two_s2 = 2.0 * sigma * sigma;
+            const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
+            for (int s = lane; s < Sb; s += 32) {
+                const double g2 = lattice_g2(a.cols, a.topo, global_unit(a, b + s * G), c);
+                const bool u2 = g2 <= r2;
+                upd[s] = u2 ? 1 : 0;
+                hs[s] = u2 ? (float)(alpha * exp(-g2 / two_s2)) : 0.0f;
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        if (s_abort) break;
+        // x_{t-1} <- x_t, x_t <- x_{t+1} (own chunks)
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            xp[j] = xc[j];
+            if (valid[j]) {
+                xc[j] = xs4[threadIdx.x + j * NT];
+                xd[j][0] = xc[j].x; xd[j][1] = xc[j].y; xd[j][2] = xc[j].z; xd[j][3] = xc[j].w;
+            }
+        }
+        __syncthreads();   // staging buffer free for the next cp.async
+    }
+
+    if (a.t1 > a.t0 && !s_abort) {
+        // flush the update of the last step (x_{t1-1} is now in xp)
+        for (int s = 0; s < Sb; ++s) {
+            if (!upd[s]) continue;
+            const float h = hs[s];
+            float4* row = W4 + (int64_t)(b + s * G) * d4;
+#pragma unroll
+            for (int j = 0; j < KJ; ++j) {
+                if (!valid[j]) continue;
+                const int c = threadIdx.x + j * NT;
+                __stcg(row + c, eq1g(h, __ldcg(row + c), xp[j]));
+            }
+        }
+    }
+}
+
+template <int KJ>
+cudaError_t launch_tma(const TrainArgs& a, int R, cudaStream_t st) {
+    const size_t smem = sizeof(float) * (size_t)a.dimp * (1 + R) + 128;
+    auto fn = som_train_tma_kernel<KJ>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    TrainArgs args = a;
+    int r = R;
+    void* params[] = {&args, &r};
+    return launch_persistent((const void*)fn, a, NT, smem, params, st);
+}
+
 template <int KJ, bool CX>
 cudaError_t launch_glb(const TrainArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float) * 2 * (size_t)a.dimp;
@@ -206,6 +403,26 @@ bool train_glb_supported(int S, int dim) {
 
 cudaError_t launch_train_glb(const TrainArgs& a, cudaStream_t st) {
     const int kj = ((a.dimp / 4) + NT - 1) / NT;
+    // TMA row ring when R >= 2 rows of the CTA fit next to the x staging buffer
+    {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const size_t rowb = sizeof(float) * (size_t)a.dimp;
+        const size_t stat = 20 * 1024;   // static smem (part/hs/upd) headroom
+        int R = (int)std::min<size_t>(4, ((size_t)optin - stat) / rowb - 1);
+        R = std::min(R, a.S);
+        if (kj <= 6 && R >= 2 && a.dim % 4 == 0 && getenv("SOM_NO_TMA_RING") == nullptr) {
+            switch (kj) {
+                case 1: return launch_tma<1>(a, R, st);
+                case 2: return launch_tma<2>(a, R, st);
+                case 3: return launch_tma<3>(a, R, st);
+                case 4: return launch_tma<4>(a, R, st);
+                case 5: return launch_tma<5>(a, R, st);
+                case 6: return launch_tma<6>(a, R, st);
+            }
+        }
+    }
     switch (kj) {
         case 1: return launch_glb<1, true>(a, st);
         case 2: return launch_glb<2, true>(a, st);

@@ -276,3 +276,16 @@ def test_c3_prefix_global_kernel(som):
         W = m.get_weights()
     Wo, logo = oracle.train_online(W0, 50, 50, 1, X, 10, 0.1, 25.0, 3, t_end=150)
     _assert_train(W, log, Wo, logo)
+
+
+@pytest.mark.parametrize("ring", [True, False])
+def test_c2_shape_global_kernels_ring_and_registers(som, monkeypatch, ring):
+    """Both global-memory kernels (TMA row ring; register-pipelined) on the
+    c2 shape agree with the oracle over 1500 steps."""
+    if not ring:
+        monkeypatch.setenv("SOM_NO_TMA_RING", "1")
+    C = bank_corpus(5000, 3000, seed=4)
+    X = C.dense()
+    W0 = init_rows(X, 400, 1004)
+    W, log, Wo, logo = _train_both(som, 20, 20, 1, X, W0, 100, 0.1, 10.0, 4, mode=2, t_end=1500)
+    _assert_train(W, log, Wo, logo)
