@@ -214,7 +214,7 @@ __device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t by
 }
 
 template <int KJ>
-__global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a, int R) {
+__global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a, int R_max) {
     __shared__ double part[kMaxSlotsG][NW];
     __shared__ float hs[kMaxSlotsG];
     __shared__ int upd[kMaxSlotsG];
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a,
     const int b = blockIdx.x, G = a.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Sb = (a.N - b + G - 1) / G;
+    const int R = Sb < R_max ? Sb : R_max;   // ring depth of this CTA (R <= Sb keeps refills final)
     const int d4 = a.dimp >> 2;
     const uint32_t row_bytes = (uint32_t)a.dim * 4u;
     float4* W4 = reinterpret_cast<float4*>(a.W);
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a,
     for (int s = threadIdx.x; s < kMaxSlotsG; s += NT) { hs[s] = 0.0f; upd[s] = 0; }
     if (threadIdx.x == 0) {
         s_abort = 0;
-        for (int r = 0; r < R; ++r) mbar_init_g(&mbar[r], 1);
+        for (int r = 0; r < R_max; ++r) mbar_init_g(&mbar[r], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
