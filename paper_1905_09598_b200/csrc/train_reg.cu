@@ -62,31 +62,15 @@ __device__ __forceinline__ double butterfly_sum(double (&v)[SMAX], int lane, int
     return x;
 }
 
-// Warp 0 coordinates (key, exchange, bookkeeping) and owns no prototype
-// chunks; warps 1..15 ("compute warps", CT = 480 threads) own chunk
-// c = (tid - 32) + j*CT of each unit.  While warp 0 waits on the exchange of
-// step t, the compute warps (i) shift x_{t+1} into registers, (ii) compute
-// the distances D_u(x_{t+1}) against the prototypes as they are now
-// ("speculative": exact for every unit the update of step t will not touch),
-// and (iii) build the neighbourhood table of step t.  After the winner is
-// known, the fused pass only applies the update and recomputes the distance
-// for units inside the neighbourhood, so late in training (small radius)
-// almost no distance work is left on the step's critical path.
-constexpr int CT = NT - 32;
-constexpr int CW = NW - 1;
-
 template <int SMAX, int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a) {
-    __shared__ double part[CW][SMAX];        // per-compute-warp partials of updated units
-    __shared__ double spec[2][CW][SMAX];     // speculative partials (double-buffered by step)
+    __shared__ double part[NW][SMAX];        // per-warp partial distance of each unit
     __shared__ int s_c;                      // winner of the current step
     __shared__ int s_abort;
     extern __shared__ __align__(16) float xring[];   // [3][dimp] x ring, then the h table
 
     const int b = blockIdx.x, G = a.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cw = warp - 1;                 // compute-warp index (-1 for warp 0)
-    const int ct = threadIdx.x - 32;         // compute-thread index
     const int Sb = (a.N - b + G - 1) / G;
     const int d4 = a.dimp >> 2;
     const float4* W4 = reinterpret_cast<const float4*>(a.W);
@@ -99,7 +83,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
 
     bool valid[KJ];
 #pragma unroll
-    for (int j = 0; j < KJ; ++j) valid[j] = warp > 0 && ct + j * CT < d4;
+    for (int j = 0; j < KJ; ++j) valid[j] = threadIdx.x + j * NT < d4;
 
     float4 w[SMAX][KJ];
     float4 xp[KJ], xc[KJ];
@@ -111,7 +95,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
 #pragma unroll
         for (int j = 0; j < KJ; ++j) {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (s < Sb && valid[j]) v = W4[(int64_t)(b + s * G) * d4 + ct + j * CT];
+            if (s < Sb && valid[j]) v = W4[(int64_t)(b + s * G) * d4 + threadIdx.x + j * NT];
             w[s][j] = v;
         }
         hh[s] = -1.0f;
@@ -127,12 +111,12 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
     if (threadIdx.x == 0) s_abort = 0;
 
     auto issue_x = [&](int64_t t) {
-        if (warp > 0 && t < a.t1) {
+        if (t < a.t1) {
             const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
             float4* dst = ring4 + (size_t)(t % 3) * d4;
 #pragma unroll
             for (int j = 0; j < KJ; ++j)
-                if (valid[j]) cp_async16(dst + ct + j * CT, src + ct + j * CT);
+                if (valid[j]) cp_async16(dst + threadIdx.x + j * NT, src + threadIdx.x + j * NT);
         }
         cp_async_commit();   // always one group per call (possibly empty)
     };
@@ -144,22 +128,38 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         for (int j = 0; j < KJ; ++j) {
             xp[j] = xc[j];
             if (valid[j]) {
-                xc[j] = src[ct + j * CT];
+                xc[j] = src[threadIdx.x + j * NT];
                 xd[j][0] = (double)xc[j].x; xd[j][1] = (double)xc[j].y;
                 xd[j][2] = (double)xc[j].z; xd[j][3] = (double)xc[j].w;
             }
         }
     };
-    // this thread's partial D_u(x) over its chunks for the units selected by `which`
-    auto partials = [&](double (&acc)[SMAX], bool all) {
+
+    issue_x(a.t0);
+    issue_x(a.t0 + 1);
+    shift_x(a.t0);            // xc = x_{t0}, xd = fp64(x_{t0})
+    __syncthreads();
+
+    for (int64_t t = a.t0; t < a.t1; ++t) {
+        unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
+        if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
+            tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
+#define TRACE(p) do { if (tr) tr[p] = globaltimer_ns(); } while (0)
+        TRACE(0);
+
+        // ---- fused pass on registers: pending update (t-1), then D_u(x_t)
+        double acc[SMAX];
 #pragma unroll
         for (int s = 0; s < SMAX; ++s) {
             acc[s] = 0.0;
-            if (s < Sb && (all || hh[s] >= 0.0f)) {
+            if (s < Sb) {
+                const float h = hh[s];
+                const bool up = h >= 0.0f;
                 double a0 = 0.0, a1 = 0.0;
 #pragma unroll
                 for (int j = 0; j < KJ; ++j) {
                     if (valid[j]) {
+                        if (up) w[s][j] = eq1u(h, w[s][j], xp[j]);
                         // R10: (double)x - (double)w, squared and summed in fp64
                         const double e0 = xd[j][0] - (double)w[s][j].x;
                         const double e1 = xd[j][1] - (double)w[s][j].y;
@@ -174,62 +174,23 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
                 acc[s] = a0 + a1;
             }
         }
-    };
-
-    issue_x(a.t0);
-    issue_x(a.t0 + 1);
-    shift_x(a.t0);            // xc = x_{t0}, xd = fp64(x_{t0})
-    if (warp > 0) {           // speculative distances of step t0 (nothing pending)
-        double acc[SMAX];
-        partials(acc, true);
-        int slot;
-        const double v = butterfly_sum<SMAX>(acc, lane, &slot);
-        if ((lane & (32 / SMAX - 1)) == 0) spec[a.t0 & 1][cw][slot] = v;
-    }
-    __syncthreads();
-
-    for (int64_t t = a.t0; t < a.t1; ++t) {
-        unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
-        if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
-            tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
-#define TRACE(p) do { if (tr) tr[p] = globaltimer_ns(); } while (0)
-        TRACE(0);
-
-        // ---- fused pass (compute warps): pending update (t-1) and the
-        // distance D_u(x_t) of the updated units; the others are speculative
-        if (warp > 0) {
-#pragma unroll
-            for (int s = 0; s < SMAX; ++s) {
-                const float h = hh[s];
-                if (s < Sb && h >= 0.0f) {
-#pragma unroll
-                    for (int j = 0; j < KJ; ++j)
-                        if (valid[j]) w[s][j] = eq1u(h, w[s][j], xp[j]);
-                }
-            }
-            double acc[SMAX];
-            partials(acc, false);
+        {
             int slot;
             const double v = butterfly_sum<SMAX>(acc, lane, &slot);
-            if ((lane & (32 / SMAX - 1)) == 0) part[cw][slot] = v;
+            if ((lane & (32 / SMAX - 1)) == 0) part[warp][slot] = v;
         }
-        issue_x(t + 2);
         TRACE(1);
+        issue_x(t + 2);
         __syncthreads();   // A: partial distances ready
         TRACE(2);
 
         if (warp == 0) {
-            // lane s sums its unit's partials (fixed order), keys, min
+            // lane s sums its unit's 16 warp partials (fixed order), keys, min
             unsigned long long key = ~0ull;
             if (lane < SMAX && lane < Sb) {
                 double tot = 0.0;
-                if (hh[lane] >= 0.0f) {
 #pragma unroll
-                    for (int w8 = 0; w8 < CW; ++w8) tot += part[w8][lane];
-                } else {
-#pragma unroll
-                    for (int w8 = 0; w8 < CW; ++w8) tot += spec[t & 1][w8][lane];
-                }
+                for (int w8 = 0; w8 < NW; ++w8) tot += part[w8][lane];
                 key = make_key((float)tot, global_unit(a, b + lane * G));
             }
 #pragma unroll
@@ -238,6 +199,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
 
             xchg_publish(a, key, t, b, lane);
             TRACE(3);
+            shift_x(t + 1);                       // hidden behind the poll
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
             const int c = key_unit(gmin);
@@ -250,22 +212,15 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
             TRACE(5);
         } else {
             shift_x(t + 1);
-            // speculative D_u(x_{t+1}) with the prototypes as of now
-            if (t + 1 < a.t1) {
-                double acc[SMAX];
-                partials(acc, true);
-                int slot;
-                const double v = butterfly_sum<SMAX>(acc, lane, &slot);
-                if ((lane & (32 / SMAX - 1)) == 0) spec[(t + 1) & 1][cw][slot] = v;
-            }
-            // neighbourhood table of step t (schedule R1-R3, kernel R4, cutoff R5)
+            // neighbourhood table of step t (schedule R1-R3, kernel R4, cutoff
+            // R5), built while warp 0 waits on the exchange
             const double f = a.f_tab[t - a.t0];
             const double alpha = a.alpha0 * f;
             double sigma = a.sigma0 * f;
             if (sigma < a.sigma_min) sigma = a.sigma_min;
             const double two_s2 = 2.0 * sigma * sigma;
             const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
-            for (int e = ct; e < HT; e += CT) {
+            for (int e = threadIdx.x - 32; e < HT; e += NT - 32) {
                 const int di = e / W2, dx = e - di * W2;
                 const double ddi = (double)di, ddx = (double)dx;
                 const double g2 = a.topo == 0 ? ddi * ddi + ddx * ddx : 0.25 * (ddx * ddx) + 0.75 * (ddi * ddi);
@@ -290,7 +245,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         }
     }
 
-    if (a.t1 > a.t0 && !s_abort && warp > 0) {
+    if (a.t1 > a.t0 && !s_abort) {
         // flush the update of the last step (x_{t1-1} is in xp)
 #pragma unroll
         for (int s = 0; s < SMAX; ++s) {
@@ -309,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         for (int s = 0; s < SMAX; ++s)
 #pragma unroll
             for (int j = 0; j < KJ; ++j)
-                if (s < Sb && valid[j]) Wo[(int64_t)(b + s * G) * d4 + ct + j * CT] = w[s][j];
+                if (s < Sb && valid[j]) Wo[(int64_t)(b + s * G) * d4 + threadIdx.x + j * NT] = w[s][j];
     }
 }
 
@@ -337,12 +292,12 @@ int smax_of(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 
 // prototype chunks plus x_{t-1}, x_t (fp32) and x_t (fp64) per chunk.
 bool train_reg_supported(int S, int dim) {
     if (dim % 4 != 0) return false;
-    const int kj = ((dim / 4) + CT - 1) / CT;
+    const int kj = ((dim / 4) + NT - 1) / NT;
     return kj <= 4 && smax_of(S) * kj <= (kj == 4 ? 4 : 8);
 }
 
 cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st) {
-    const int kj = ((a.dimp / 4) + CT - 1) / CT;
+    const int kj = ((a.dimp / 4) + NT - 1) / NT;
     const int sm = smax_of(a.S);
 #define TRY(SM, K) if (sm == SM && kj == K) return launch_one<SM, K>(a, st)
     TRY(1, 1); TRY(2, 1); TRY(4, 1); TRY(8, 1);
