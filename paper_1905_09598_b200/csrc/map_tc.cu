@@ -16,8 +16,8 @@
 // K=8 per instruction, 12 instructions per 32-wide K-block), warps 2-5 =
 // epilogue: tcgen05.ld 32 accumulator columns at a time, D in fp32, running
 // top-2 (D, u) per document row across all unit tiles of the work item.
-// Two TMEM accumulators (2 x BN columns) let the epilogue of one unit tile
-// overlap the MMAs of the next.  A work item is (128-document block, range
+// Two TMEM accumulators (2 x BN columns) hold the hi.hi products and the
+// two small lo products separately (accuracy: see the MMA loop).  A work item is (128-document block, range
 // of unit tiles); its partial top-2 keys go to the same merge kernel as the
 // exact path.
 #include <cuda.h>
@@ -38,7 +38,7 @@ constexpr int TC_THREADS = 192;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;            // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;            // 32 KB
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
-constexpr uint32_t TMEM_COLS = 2 * TC_BN;                  // two accumulators
+constexpr uint32_t TMEM_COLS = 2 * TC_BN;                  // hh and lo accumulators
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -210,10 +210,14 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
         uint32_t tile = 0;
         for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x, ++tile) {
             {
-                const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
+                // one tile in flight: accumulator hh (x_hi.w_hi) at column 0 and
+                // lo (x_lo.w_hi + x_hi.w_lo) at column BN, so the large
+                // accumulator takes K/8 adds instead of 3K/8 (its fp32
+                // accumulation is not round-to-nearest)
+                const uint32_t buf = 0, tph = tile & 1;
                 mbar_wait(&tempty[buf], tph ^ 1);
                 tc_fence_after();
-                const uint32_t tmem_d = tmem_base + buf * TC_BN;
+                const uint32_t acc_hh = tmem_base, acc_lo = tmem_base + TC_BN;
                 for (int kb = 0; kb < a.kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -225,9 +229,9 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
                         for (int k = 0; k < TC_BK / 8; ++k) {
                             const uint64_t ko = (uint64_t)((k * 32) >> 4);   // +32 B per K=8 step
                             const uint32_t acc0 = (kb | k) != 0;
-                            mma_tf32(tmem_d, alo + ko, bhi + ko, idesc, acc0);   // small terms first
-                            mma_tf32(tmem_d, ahi + ko, blo + ko, idesc, 1u);
-                            mma_tf32(tmem_d, ahi + ko, bhi + ko, idesc, 1u);
+                            mma_tf32(acc_lo, alo + ko, bhi + ko, idesc, acc0);
+                            mma_tf32(acc_lo, ahi + ko, blo + ko, idesc, 1u);
+                            mma_tf32(acc_hh, ahi + ko, bhi + ko, idesc, acc0);
                         }
                         mma_commit(&empty[stage]);                   // smem slot free when these MMAs finish
                         if (kb == a.kblocks - 1) mma_commit(&tfull[buf]);
@@ -250,14 +254,17 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
             float d1 = INFINITY, d2 = INFINITY;
             int u1 = -1, u2 = -1;
             {
-                const uint32_t buf = tile & 1, tph = (tile >> 1) & 1;
+                const uint32_t buf = 0, tph = tile & 1;
                 mbar_wait(&tfull[buf], tph);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * TC_BN;
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
                 for (int c = 0; c < TC_BN / 32; ++c) {
-                    float v[32];
+                    float v[32], vl[32];
                     tmem_ld32(taddr + c * 32, v);
+                    tmem_ld32(taddr + TC_BN + c * 32, vl);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] += vl[i];
                     const int u0 = nt * TC_BN + c * 32;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
