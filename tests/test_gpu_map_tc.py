@@ -37,8 +37,9 @@ def _check(b1, b2, d1, ob1, ob2, od1, m12, m23):
     bad2 = np.flatnonzero(ok2 & (b2 != ob2))
     assert bad2.size == 0, f"bmu2 differs on {bad2.size} docs"
     # D1: tensor-core fp32 accumulation is not round-to-nearest (observed
-    # positive bias growing with K); bar 2e-5 absolute, 5x inside
-    # the north star's 1e-4 max-abs for errors.
+    # positive bias growing with K). With the hi.hi and lo
+    # products in separate TMEM accumulators the observed max is ~5e-6; bar
+    # 1e-5 absolute, 10x inside the north star's 1e-4 max-abs for errors.
     ab = np.abs(d1.astype(np.float64) - od1)
     assert ab.max() <= 1e-5, ab.max()
     print(f" [3xTF32 D1 abs err max {ab.max():.2e} median {np.median(ab):.2e}]", end="")
