@@ -117,6 +117,22 @@ som_status som_train_online(som_ctx *h, const float *X, int64_t n, int32_t epoch
                             uint64_t seed, int64_t t_begin, int64_t t_end,
                             int32_t *bmu_log);
 
+/* som_train_online on CSR input (int64 rowptr[n+1] from 0, non-decreasing;
+ * int32 col strictly increasing within a row, in [0, dim); fp32 val — the
+ * sparse TF-IDF rows of P:148-154).  Same steps, same
+ * results as som_train_online on the dense rows: identical BMU log and
+ * weights (the dense oracle is the parity reference).  Where W streams from
+ * global memory (kernel 4 in som_last_train_config), units outside the
+ * cutoff radius of the pending update get
+ *   D_u = |w_u|^2 + sum_{k in nz(x)} ((x_k - w_uk)^2 - w_uk^2)
+ * in fp64 (R25) instead of a dense pass, with |w_u|^2 kept in fp64 by the
+ * update pass; smaller maps train on the densified rows.  A malformed CSR
+ * returns SOM_EINVAL before any side effect (checked on the device). */
+som_status som_train_online_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
+                                const float *val, int64_t n, int32_t epochs, double alpha0,
+                                double sigma0, const som_schedule *s, uint64_t seed,
+                                int64_t t_begin, int64_t t_end, int32_t *bmu_log);
+
 /* Where som_train_online keeps each CTA's prototypes between steps:
  * AUTO picks shared memory when a CTA's share of W fits (else global
  * memory, L2-resident when W fits the L2); REGISTERS keeps each CTA's share
@@ -134,7 +150,8 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
 
 /* Grid and kernel variant of the last som_train_online call:
  * kernel 0 = W in global memory (generic), 1 = W in shared memory,
- * 2 = W in registers, 3 = W in global memory (pipelined, d % 4 == 0). */
+ * 2 = W in registers, 3 = W in global memory (pipelined, d % 4 == 0),
+ * 4 = W in global memory with the sparse distance path (CSR input). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* ---- Neuron sharding: online training of one map across
@@ -177,6 +194,8 @@ som_status som_set_trace(som_ctx *h, void *device_buf, int32_t steps);
  * Euclidean, fp32).  bmu2, d2 nullable.  Precision per som_set_map_precision. */
 som_status som_map(som_ctx *h, const float *X, int64_t n, int32_t *bmu1, int32_t *bmu2,
                    float *d2);
+/* som_map_csr: CSR rows as in som_train_online_csr (validated on the
+ * device, SOM_EINVAL when malformed). */
 som_status som_map_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
                        const float *val, int64_t n, int32_t *bmu1, int32_t *bmu2,
                        float *d2);

@@ -335,32 +335,109 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     return SOM_OK;
 }
 
-som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epochs, double alpha0, double sigma0,
-                            const som_schedule* s, uint64_t seed, int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
-    CHECK_HANDLE(h);
-    som_schedule sd;
-    som_schedule_default(&sd);
-    if (s) sd = *s;
-    if (!X) return fail(SOM_EINVAL, "null X");
+namespace {
+
+struct CsrIn {
+    const int64_t* rowptr;
+    const int32_t* col;
+    const float* val;
+    int maxnnz;
+};
+
+// shared argument checks of som_train_online / som_train_online_csr; on OK
+// *sd holds the schedule and [*t_begin, *t_end) the (resolved) step range
+som_status check_train(som_ctx* h, int64_t n, int32_t epochs, double alpha0, double sigma0, const som_schedule* s,
+                       som_schedule* sd, int64_t* t_begin, int64_t* t_end) {
+    som_schedule_default(sd);
+    if (s) *sd = *s;
     if (n < 1) return fail(SOM_EEMPTY, "n = 0: no data to train on");
     if (epochs < 0) return fail(SOM_EINVAL, "epochs must be >= 0");
     if (!(alpha0 >= 0.0 && alpha0 <= 1.0)) return fail(SOM_EINVAL, "alpha0 must be in [0, 1]");
     if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
-    if (sd.kind < 0 || sd.kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
-    if (!(sd.k > 0.0) || !std::isfinite(sd.k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
-    if (!(sd.sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
-    if (!(sd.cutoff >= 0.0 && sd.cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
+    if (sd->kind < 0 || sd->kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
+    if (!(sd->k > 0.0) || !std::isfinite(sd->k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
+    if (!(sd->sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
+    if (!(sd->cutoff >= 0.0 && sd->cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
     const int64_t T = (int64_t)epochs * n;
-    if (t_end == -1) t_end = T;
-    if (t_begin < 0 || t_end < t_begin || t_end > T) return fail(SOM_EINVAL, "bad t-range [%lld, %lld) for T = %lld",
-                                                                 (long long)t_begin, (long long)t_end, (long long)T);
+    if (*t_end == -1) *t_end = T;
+    if (*t_begin < 0 || *t_end < *t_begin || *t_end > T)
+        return fail(SOM_EINVAL, "bad t-range [%lld, %lld) for T = %lld", (long long)*t_begin, (long long)*t_end,
+                    (long long)T);
     h->last_ms = 0; h->last_units = 0; h->last_launches = 0;
-    if (t_end == t_begin) return SOM_OK;   // epochs = 0 or empty range: weights unchanged (S:221)
-    h->w_split_valid = false;
+    return SOM_OK;
+}
 
-    const void* Xd = nullptr;
-    som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
+// CSR arrays staged to the device and checked there (rowptr from 0 and
+// non-decreasing, col strictly increasing within a row and < dim); returns
+// the device pointers and the largest row length
+som_status stage_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                     CsrIn* out) {
+    if (!rowptr || !col || !val) return fail(SOM_EINVAL, "null CSR array");
+    int64_t nnz = 0;
+    if (is_device_ptr(rowptr)) CK(cudaMemcpy(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    else nnz = rowptr[n];
+    if (nnz < 0) return fail(SOM_EINVAL, "rowptr[n] < 0");
+    const void *rpd, *cd, *vd;
+    som_status st = stage_in(h, h->xin, rowptr, sizeof(int64_t) * (size_t)(n + 1), &rpd);
     if (st) return st;
+    if ((st = stage_in(h, h->xin2, col, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1), &cd))) return st;
+    if ((st = stage_in(h, h->xin3, val, sizeof(float) * (size_t)std::max<int64_t>(nnz, 1), &vd))) return st;
+    CK(h->red.ensure(64, h->stream));
+    int* chk = (int*)h->red.p;
+    CK(launch_csr_check((const int64_t*)rpd, (const int32_t*)cd, n, h->dim, chk, h->stream));
+    int res[2] = {0, 0};
+    CK(cudaMemcpyAsync(res, chk, sizeof(res), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (res[0] & 1) return fail(SOM_EINVAL, "CSR rowptr must start at 0 and be non-decreasing");
+    if (res[0] & 2) return fail(SOM_EINVAL, "CSR column index outside [0, dim)");
+    if (res[0] & 4) return fail(SOM_EINVAL, "CSR column indices must be strictly increasing within a row");
+    out->rowptr = (const int64_t*)rpd;
+    out->col = (const int32_t*)cd;
+    out->val = (const float*)vd;
+    out->maxnnz = res[1];
+    return SOM_OK;
+}
+
+som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, int32_t epochs, double alpha0,
+                      double sigma0, const som_schedule& sd, uint64_t seed, int64_t t_begin, int64_t t_end,
+                      int32_t* bmu_log);
+
+}  // namespace
+
+som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epochs, double alpha0, double sigma0,
+                            const som_schedule* s, uint64_t seed, int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
+    CHECK_HANDLE(h);
+    if (!X) return fail(SOM_EINVAL, "null X");
+    som_schedule sd;
+    som_status st = check_train(h, n, epochs, alpha0, sigma0, s, &sd, &t_begin, &t_end);
+    if (st) return st;
+    if (t_end == t_begin) return SOM_OK;   // epochs = 0 or empty range: weights unchanged (S:221)
+    const void* Xd = nullptr;
+    if ((st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd))) return st;
+    return train_impl(h, Xd, nullptr, n, epochs, alpha0, sigma0, sd, seed, t_begin, t_end, bmu_log);
+}
+
+som_status som_train_online_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                                int32_t epochs, double alpha0, double sigma0, const som_schedule* s, uint64_t seed,
+                                int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
+    CHECK_HANDLE(h);
+    som_schedule sd;
+    som_status st = check_train(h, n, epochs, alpha0, sigma0, s, &sd, &t_begin, &t_end);
+    if (st) return st;
+    CsrIn csr{};
+    if ((st = stage_csr(h, rowptr, col, val, n, &csr))) return st;
+    if (t_end == t_begin) return SOM_OK;
+    return train_impl(h, nullptr, &csr, n, epochs, alpha0, sigma0, sd, seed, t_begin, t_end, bmu_log);
+}
+
+namespace {
+
+som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, int32_t epochs, double alpha0,
+                      double sigma0, const som_schedule& sd, uint64_t seed, int64_t t_begin, int64_t t_end,
+                      int32_t* bmu_log) {
+    const int64_t T = (int64_t)epochs * n;
+    h->w_split_valid = false;
+    som_status st = SOM_OK;
     if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
 
     TrainArgs a{};
@@ -372,7 +449,7 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
         for (int p = 0; p < h->world; ++p)
             if (!h->peer_mail[p]) return fail(SOM_ESTATE, "neuron sharding: peer mailboxes not set (som_comm_set_peers_*)");
     }
-    a.x_vec4 = (h->dim % 4 == 0) && ((uintptr_t)Xd % 16 == 0);
+    a.x_vec4 = (h->dim % 4 == 0) && (csr || (uintptr_t)Xd % 16 == 0);   // densified CSR is aligned
     // launch geometry.  Register-resident kernel when a CTA's share of W fits
     // the register file: G minimises (all-gather latency + fp64 distance
     // time), both measured on B200 (profiles/probe_*_r01.json).  Otherwise
@@ -424,6 +501,22 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     const bool use_glb = !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
     if (use_reg) smem = sizeof(float) * (3 * (size_t)a.dimp + (size_t)a.rows * (a.topo == 0 ? a.cols : 2 * a.cols));
     if (use_glb) smem = sizeof(float) * 2 * (size_t)a.dimp;
+    // CSR input: the sparse-distance kernel where W streams from global
+    // memory; on-chip maps (latency-bound, no gain) and layouts it does not
+    // cover train on the densified rows
+    bool use_csr = false;
+    if (csr) {
+        use_csr = !use_reg && !a.w_smem && train_csr_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin);
+        if (use_csr) {
+            a.rowptr = csr->rowptr; a.col = csr->col; a.val = csr->val;
+            a.nz_cap = csr_nz_cap(csr->maxnnz);
+            smem = sizeof(float) * 2 * (size_t)a.dimp + 24 * (size_t)a.nz_cap;
+        } else {
+            CK(h->dense.ensure(sizeof(float) * (size_t)n * h->dim, h->stream));
+            CK(launch_densify(csr->rowptr, csr->col, csr->val, 0, n, h->dim, (float*)h->dense.p, h->stream));
+            a.X = (const float*)h->dense.p;
+        }
+    }
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
 
@@ -463,6 +556,7 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     }
     CK(cudaEventRecord(h->ev0, h->stream));
     if (use_reg) CK(launch_train_reg(a, h->stream));
+    else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
@@ -474,7 +568,7 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_reg ? 2 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -496,6 +590,8 @@ som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epoch
     h->last_ms = ms; h->last_units = steps; h->last_launches = 1;
     return SOM_OK;
 }
+
+}  // namespace
 
 som_status som_comm_init(som_ctx* h, int32_t rank, int32_t world) {
     CHECK_HANDLE(h);
@@ -752,18 +848,13 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
         return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
     if (n < 0) return fail(SOM_EINVAL, "n < 0");
     if (n == 0) return SOM_OK;
-    if (!rowptr || !col || !val || !bmu1) return fail(SOM_EINVAL, "null CSR array or bmu1");
-    // nnz from rowptr[n] (host or device)
-    int64_t nnz = 0;
-    const bool rp_dev = is_device_ptr(rowptr);
-    if (rp_dev) CK(cudaMemcpy(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    else nnz = rowptr[n];
-    if (nnz < 0) return fail(SOM_EINVAL, "rowptr[n] < 0");
-    const void *rpd, *cd, *vd;
-    som_status st = stage_in(h, h->xin, rowptr, sizeof(int64_t) * (size_t)(n + 1), &rpd);
+    if (!bmu1) return fail(SOM_EINVAL, "null bmu1");
+    CsrIn csr{};
+    som_status st = stage_csr(h, rowptr, col, val, n, &csr);
     if (st) return st;
-    if ((st = stage_in(h, h->xin2, col, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1), &cd))) return st;
-    if ((st = stage_in(h, h->xin3, val, sizeof(float) * (size_t)std::max<int64_t>(nnz, 1), &vd))) return st;
+    const void* rpd = csr.rowptr;
+    const void* cd = csr.col;
+    const void* vd = csr.val;
     OutStage o;
     if ((st = stage_outputs(h, n, bmu1, bmu2, d2, false, o))) return st;
     if (use_tc(h, n)) {

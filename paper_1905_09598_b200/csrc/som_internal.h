@@ -43,6 +43,11 @@ struct TrainArgs {
     // every rank p (peer memory over NVLink) and all CTAs poll mail[rank].
     int rank, world;
     unsigned long long* mail[8];
+    // CSR input (train_csr.cu): x_t = row sample_at(t) of (rowptr, col, val)
+    const int64_t* rowptr;
+    const int32_t* col;
+    const float* val;
+    int nz_cap;                // per-step (col, val) list capacity in smem
 };
 
 constexpr int kTracePhases = 8;
@@ -147,6 +152,15 @@ cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st);
 // pipelined global-memory variant (train_glb.cu) for maps that do not fit on chip
 bool train_glb_supported(int S, int dim);
 cudaError_t launch_train_glb(const TrainArgs& a, cudaStream_t st);
+
+// CSR-input variant with the sparse distance path (train_csr.cu)
+int csr_nz_cap(int maxnnz);
+bool train_csr_supported(int S, int dim, int maxnnz, int max_smem_optin);
+cudaError_t launch_train_csr(const TrainArgs& a, cudaStream_t st);
+// CSR validation: out[0] error bits (1 rowptr, 2 col range, 4 col order),
+// out[1] max nonzeros per row (device ints)
+cudaError_t launch_csr_check(const int64_t* rowptr, const int32_t* col, int64_t n, int dim, int* out,
+                             cudaStream_t st);
 
 // Exact (fp64-accumulated) batch mapping: partial top-2 keys per doc per
 // neuron split, then merged.  keys: [nsplit][n][2] u64 scratch.

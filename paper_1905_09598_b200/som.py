@@ -42,7 +42,7 @@ _lib = None
 
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
-           "som_init_random", "som_train_online", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
            "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
            "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
@@ -64,6 +64,7 @@ def lib():
         "som_get_weights": [P, P],
         "som_init_random": [P, P, i64, u64],
         "som_train_online": [P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
+        "som_train_online_csr": [P, P, P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
         "som_map": [P, P, i64, P, P, P],
         "som_map_csr": [P, P, P, P, i64, P, P, P],
         "som_set_map_precision": [P, i32],
@@ -160,6 +161,15 @@ def som_train_online(h, X, n: int, epochs: int, alpha0: float, sigma0: float, sc
     sp = ctypes.byref(sched) if sched is not None else None
     _check(lib().som_train_online(h, _ptr(X, np.float32), n, epochs, alpha0, sigma0, sp, seed & (2**64 - 1),
                                   t_begin, t_end, _ptr(bmu_log, np.int32, writable=True)))
+
+
+def som_train_online_csr(h, rowptr, col, val, n: int, epochs: int, alpha0: float, sigma0: float,
+                         sched: som_schedule | None, seed: int, t_begin: int = 0, t_end: int = -1,
+                         bmu_log=None) -> None:
+    sp = ctypes.byref(sched) if sched is not None else None
+    _check(lib().som_train_online_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                                      epochs, alpha0, sigma0, sp, seed & (2**64 - 1), t_begin, t_end,
+                                      _ptr(bmu_log, np.int32, writable=True)))
 
 
 def som_map(h, X, n: int, bmu1, bmu2=None, d2=None) -> None:
@@ -314,6 +324,16 @@ class SOM:
             sigma0 = max(self.rows, self.cols) / 2.0
         s = som_schedule(kind, k, sigma_min, cutoff)
         som_train_online(self.h, X, X.shape[0], epochs, alpha0, sigma0, s, seed, t_begin, t_end, bmu_log)
+        return bmu_log
+
+    def train_online_csr(self, rowptr, col, val, n: int, epochs: int, alpha0: float = 0.1,
+                         sigma0: float | None = None, seed: int = 1, kind: int = SOM_DECAY_GAUSSIAN,
+                         k: float = math.log(100.0), sigma_min: float = 1.0, cutoff: float = 1e-4,
+                         t_begin: int = 0, t_end: int = -1, bmu_log=None):
+        if sigma0 is None:
+            sigma0 = max(self.rows, self.cols) / 2.0
+        s = som_schedule(kind, k, sigma_min, cutoff)
+        som_train_online_csr(self.h, rowptr, col, val, n, epochs, alpha0, sigma0, s, seed, t_begin, t_end, bmu_log)
         return bmu_log
 
     def map(self, X, want_bmu2: bool = True, want_d2: bool = True):
