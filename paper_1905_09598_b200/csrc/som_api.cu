@@ -90,6 +90,8 @@ struct som_ctx {
     DevBuf log;      // staged BMU log
     DevBuf xchg;     // per-CTA exchange slots + abort flag
     DevBuf dense;    // densified CSR chunk
+    DevBuf utab;     // unit dealing of the CSR training kernels: [G][S] + counts[G]
+    int utab_G = 0, utab_NL = 0, utab_rank = -1, utab_world = 0;
     DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp32)
     DevBuf xsplit;   // tensor-core mapping: X chunk hi | lo | |x|^2
     bool w_split_valid = false;
@@ -252,7 +254,7 @@ void som_destroy(som_ctx* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
-                      &h->wsplit, &h->xsplit})
+                      &h->utab, &h->wsplit, &h->xsplit})
         b->release();
     if (h->W) cudaFree(h->W);
     for (int p = 0; p < kMaxRanks; ++p)
@@ -365,6 +367,44 @@ som_status check_train(som_ctx* h, int64_t n, int32_t epochs, double alpha0, dou
                     (long long)T);
     h->last_ms = 0; h->last_units = 0; h->last_launches = 0;
     return SOM_OK;
+}
+
+// Unit dealing for the CSR training kernels.  With cyclic dealing (b + s*G)
+// the units of one CTA lie on a few long lattice lines, so the disk of units
+// a pending update touches gives some CTAs many rows and others none, and the
+// step waits for the fullest CTA.  Here unit (i, j) goes to class
+// (alpha*i + j) mod G with alpha chosen so that every class is a near-square
+// sub-lattice (its shortest vector is maximal), then to the first class with
+// room (capacity ceil(NL/G), linear probing): any disk then holds about the
+// same number of rows of every CTA, and the all-dense step keeps its balance.
+void build_unit_tab(int rows, int cols, int topo, int rank, int world, int NL, int G, std::vector<int>& out) {
+    const int S = (NL + G - 1) / G;
+    int best_alpha = cols % G;
+    double best_len = -1.0;
+    for (int al = 1; al < G; ++al) {
+        double mn = 1e300;
+        for (int di = 0; di < rows && di <= 64; ++di) {
+            const int dj0 = (int)((((long long)-al * di) % G + G) % G);
+            for (int dj : {dj0, dj0 - G}) {
+                if (di == 0 && dj == 0) continue;
+                if (dj >= cols || -dj >= cols) continue;   // no such pair of units
+                const double len = topo == 0 ? (double)di * di + (double)dj * dj
+                                             : (double)dj * dj + 0.75 * (double)di * di;
+                mn = std::min(mn, len);
+            }
+        }
+        if (mn > best_len) { best_len = mn; best_alpha = al; }
+    }
+    out.assign((size_t)G * S + G, -1);
+    int* cnt = out.data() + (size_t)G * S;
+    for (int b = 0; b < G; ++b) cnt[b] = 0;
+    for (int l = 0; l < NL; ++l) {
+        const long long u = (long long)rank + (long long)world * l;
+        const long long i = u / cols, j = u % cols;
+        int k = (int)(((long long)best_alpha * i + j) % G);
+        while (cnt[k] >= S) k = (k + 1) % G;
+        out[(size_t)k * S + cnt[k]++] = l;
+    }
 }
 
 // CSR arrays staged to the device and checked there (rowptr from 0 and
@@ -510,6 +550,20 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         if (use_csr) {
             a.rowptr = csr->rowptr; a.col = csr->col; a.val = csr->val;
             a.nz_cap = csr_nz_cap(csr->maxnnz);
+            // upper bound of the lattice g2 between any two units (exact for
+            // rect; hex bound takes the half-column offset at the full row span)
+            const double dr = h->rows - 1, dc = h->cols - 1;
+            a.g2max = h->topo == 0 ? dr * dr + dc * dc : 0.25 * (2 * dc + 1) * (2 * dc + 1) + 0.75 * dr * dr;
+            if (h->utab_G != a.G || h->utab_NL != h->NL || h->utab_rank != h->rank || h->utab_world != h->world) {
+                std::vector<int> tab;
+                build_unit_tab(h->rows, h->cols, h->topo, h->rank, h->world, h->NL, a.G, tab);
+                CK(h->utab.ensure(sizeof(int) * tab.size(), h->stream));
+                CK(cudaMemcpyAsync(h->utab.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+                h->utab_G = a.G; h->utab_NL = h->NL; h->utab_rank = h->rank; h->utab_world = h->world;
+            }
+            a.utab = (const int*)h->utab.p;
+            a.ucnt = a.utab + (size_t)a.G * a.S;
             smem = sizeof(float) * 2 * (size_t)a.dimp + 24 * (size_t)a.nz_cap;
         } else {
             CK(h->dense.ensure(sizeof(float) * (size_t)n * h->dim, h->stream));

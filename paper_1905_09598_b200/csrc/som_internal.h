@@ -48,6 +48,11 @@ struct TrainArgs {
     const int32_t* col;
     const float* val;
     int nz_cap;                // per-step (col, val) list capacity in smem
+    double g2max;              // largest lattice g2 between two units of the map
+    // optional unit dealing (train_csr.cu): CTA b owns local units
+    // utab[b * S + s], s < ucnt[b]; NULL = cyclic (b + s * G)
+    const int* utab;
+    const int* ucnt;
 };
 
 constexpr int kTracePhases = 8;

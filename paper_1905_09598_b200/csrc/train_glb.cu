@@ -195,24 +195,6 @@ __global__ void __launch_bounds__(NT, 1) som_train_glb_kernel(const TrainArgs a)
 // CTA's sequence (q = step * Sb + s) lives in buffer q % R; the refill of
 // buffer q % R with row q + R is issued only after row q was processed and
 // written back (R <= Sb, so row q + R is final at that point).
-__device__ __forceinline__ void mbar_init_g(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAITG_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITG_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    const unsigned sb = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"(sb) : "memory");
-}
-
 template <int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a, int R_max) {
     __shared__ double part[kMaxSlotsG][NW];
