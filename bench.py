@@ -138,10 +138,26 @@ def tf32_peak_tflops():
     return 1590.0 * 1.1 / 2.25, "fallback bf16 1590 TFLOP/s x 1.1/2.25 (B200_PROFILING.md)"
 
 
+def conv_peak_per_s():
+    """fp32 -> fp64 conversions per second (F2F.F64.F32, the bound of the
+    fp32-stored sparse mapping kernel and of the training distance): the
+    measured per-SM rate (profiles/probe_fp64.json) x 148 SMs x max clock."""
+    path = os.path.join(ROOT, "profiles", "probe_fp64.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        return j["train_element_peak_per_s"], (f"measured F2F.F64.F32 rate {j['f2f_per_clk_per_sm']}/clk/SM x 148 "
+                                               "SMs x 1965 MHz (profiles/probe_fp64.json)")
+    return 16 * 148 * 1965e6, "nominal 16 F2F/clk/SM x 148 x 1965 MHz (no measurement file)"
+
+
 def mapping_leg(som, torch, args, local, seed):
     """Batch BMU mapping docs/s on a c5-shaped sample (BASELINE.json configs[4]:
     100x100 map, 20k terms, CSR documents; the full 10M-document job is the
-    doc-sharded multi-GPU case) through som_map_csr on the tcgen05 path."""
+    doc-sharded multi-GPU case) through som_map_csr.  Main: the default (AUTO)
+    path, the exact fp64 sparse identity (map_sparse.cu, R25); beside it the
+    dense tcgen05 3xTF32 contraction (map_tc.cu) on the same documents, and
+    the oracle's sparse-identity mapping on the host cores for a sample."""
     cfg = CONFIGS["c5"]
     n, d, N = args.map_docs, cfg["d"], cfg["rows"] * cfg["cols"]
     C = bank_corpus(n, d, seed=seed + 500)
@@ -151,31 +167,61 @@ def mapping_leg(som, torch, args, local, seed):
     mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
     som.som_set_stream(mm.h, torch.cuda.current_stream())
     mm.set_weights(torch.from_numpy(W).cuda())
-    som.som_set_map_precision(mm.h, som.SOM_MAP_3XTF32)
     rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
     b1 = torch.empty(n, dtype=torch.int32, device="cuda")
     b2 = torch.empty(n, dtype=torch.int32, device="cuda")
     d1 = torch.empty(n, dtype=torch.float32, device="cuda")
-    som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)          # warm-up (W split, scratch)
-    times, kern = [], []
-    for _ in range(max(1, args.steps)):
-        torch.cuda.synchronize()
-        som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)
-        ms, _, launches = som.som_last_stats(mm.h)
-        times.append(ms)
-        kern.append(launches)
-    ms = statistics.mean(times)
+
+    def timed(precision):
+        som.som_set_map_precision(mm.h, precision)
+        som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)          # warm-up (W^T / W split, scratch)
+        times, kern = [], []
+        for _ in range(max(3, args.steps)):
+            torch.cuda.synchronize()
+            som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)
+            ms, _, launches = som.som_last_stats(mm.h)
+            times.append(ms)
+            kern.append(launches)
+        return statistics.mean(times), kern[-1]
+
+    ms, launches = timed(som.SOM_MAP_AUTO)
+    sp_b1 = b1.cpu().numpy()
+    ms_tc, launches_tc = timed(som.SOM_MAP_3XTF32)
+    agree = float(np.mean(b1.cpu().numpy() == sp_b1))
+    mm.close()
+    fma = float(C.nnz) * N
+    cpk, cpk_src = conv_peak_per_s()
     flop = 2.0 * n * N * d
     peak, src = tf32_peak_tflops()
-    executed = 3.0 * flop / (ms / 1000.0) / 1e12
-    mm.close()
+    executed = 3.0 * flop / (ms_tc / 1000.0) / 1e12
+
+    cpu = None
+    if not args.no_baseline:
+        import oracle
+        ns = min(n, 10000)
+        t0 = time.perf_counter()
+        oracle.map_docs_csr(W, C.indptr[:ns + 1], C.indices[:C.indptr[ns]], C.data[:C.indptr[ns]])
+        dt = time.perf_counter() - t0
+        cpu = {"value": ns / dt, "unit": "docs/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": f"first {ns} documents, fp64 sparse-identity oracle (or_map_csr, OpenMP over docs), "
+                         f"{dt:.1f} s"}
     return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms",
-            "docs_per_s": n / (ms / 1000.0), "ms": ms, "launches": kern[-1],
-            "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
-                         "achieved": executed, "peak": peak, "unit": "TFLOP/s", "frac": executed / peak,
-                         "peak_source": src,
-                         "work": "3 x 2*n*N*d executed TF32 flop per call (3xTF32 split), incl. CSR split + merge",
-                         "algorithmic_fp32_tflops": flop / (ms / 1000.0) / 1e12}}
+            "docs_per_s": n / (ms / 1000.0), "ms": ms, "launches": launches,
+            "path": "exact fp64 sparse identity (SOM_MAP_SPARSE_F64, AUTO)",
+            "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T>",
+                         "achieved": fma / (ms / 1000.0) / 1e12, "peak": cpk / 1e12, "unit": "T conv+FMA/s",
+                         "frac": fma / (ms / 1000.0) / cpk, "peak_source": cpk_src,
+                         "work": "nnz*N fp32->fp64 conversions + fp64 FMAs per call (one per non-zero per unit), "
+                                 "incl. the top-2 merge kernel"},
+            "cpu_baseline": cpu,
+            "tc_3xtf32": {"docs_per_s": n / (ms_tc / 1000.0), "ms": ms_tc, "launches": launches_tc,
+                          "bmu1_agreement_with_exact": agree,
+                          "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
+                                       "achieved": executed, "peak": peak, "unit": "TFLOP/s",
+                                       "frac": executed / peak, "peak_source": src,
+                                       "work": "3 x 2*n*N*d executed TF32 flop per call (3xTF32 split), incl. "
+                                               "CSR split + merge",
+                                       "algorithmic_fp32_tflops": flop / (ms_tc / 1000.0) / 1e12}}}
 
 
 def updated_units(rows, cols, topo, bmu_log, t0, T, sigma0, eps=1e-4, k=math.log(100.0), sigma_min=1.0):

@@ -79,7 +79,9 @@ typedef struct {
 typedef enum {
     SOM_MAP_AUTO = 0,      /* fastest path available on the device          */
     SOM_MAP_EXACT_F64 = 1, /* fp64-accumulated direct distances (= oracle)   */
-    SOM_MAP_3XTF32 = 2     /* tcgen05 3xTF32 GEMM |x|^2 - 2 x.w + |w|^2 (R20) */
+    SOM_MAP_3XTF32 = 2,    /* tcgen05 3xTF32 GEMM |x|^2 - 2 x.w + |w|^2 (R20) */
+    SOM_MAP_SPARSE_F64 = 3 /* CSR rows: fp64 sparse identity over the
+                              non-zeros of x (R25); dense rows: as EXACT_F64 */
 } som_map_precision;
 
 /* Fill *s with the defaults above. */
@@ -199,6 +201,9 @@ som_status som_map(som_ctx *h, const float *X, int64_t n, int32_t *bmu1, int32_t
 som_status som_map_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
                        const float *val, int64_t n, int32_t *bmu1, int32_t *bmu2,
                        float *d2);
+/* Precision / algorithm of the mapping calls (som_map_precision).  AUTO:
+ * CSR rows with <= 1.5 % of the terms set take SOM_MAP_SPARSE_F64; other
+ * inputs take EXACT_F64, or 3XTF32 once n*N*dim >= 1e10. */
 som_status som_set_map_precision(som_ctx *h, int32_t precision);
 
 /* Quantization error (R14; Table 2): mean over rows of
@@ -207,8 +212,11 @@ som_status som_qerror(som_ctx *h, const float *X, int64_t n, double *qe);
 /* Topographic error (R15; BJ:5): fraction of rows whose two best units are
  * not lattice-adjacent (g2 != 1; 0 for a 1-unit map).  n >= 1. */
 som_status som_topographic_error(som_ctx *h, const float *X, int64_t n, double *te);
-/* Both errors from one mapping pass. */
+/* Both errors from one mapping pass.  qe, te nullable. */
 som_status som_errors(som_ctx *h, const float *X, int64_t n, double *qe, double *te);
+/* The same for CSR rows (validated as in som_map_csr). */
+som_status som_errors_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
+                          const float *val, int64_t n, double *qe, double *te);
 
 /* U-matrix (R16; BJ:5): U_u = mean over lattice-adjacent v (g2 = 1) of
  * |w_u - w_v|_2 (fp64 accumulation, fp32 result), 0 with no neighbour.

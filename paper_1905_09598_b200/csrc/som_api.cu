@@ -95,6 +95,9 @@ struct som_ctx {
     DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp32)
     DevBuf xsplit;   // tensor-core mapping: X chunk hi | lo | |x|^2
     bool w_split_valid = false;
+    DevBuf wt64;     // sparse mapping: W^T fp64 or fp32 (dim x Np) | |W|^2 fp64 (N)
+    bool wt_valid = false, wt_f32 = false;
+    int wt_J = 0;
     // decay-table cache
     int64_t f_T = -1, f_t0 = -1, f_t1 = -1;
     int f_kind = -1;
@@ -117,6 +120,12 @@ namespace {
                         #call, cudaGetErrorString(e_), __FILE__, __LINE__);                   \
         }                                                                                     \
     } while (0)
+
+// W changed: drop every derived copy (tensor-core split planes, sparse W^T)
+void invalidate_w_caches(som_ctx* h) {
+    h->w_split_valid = false;
+    h->wt_valid = false;
+}
 
 #define CHECK_HANDLE(h)                                                                       \
     do {                                                                                      \
@@ -254,7 +263,7 @@ void som_destroy(som_ctx* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
-                      &h->utab, &h->wsplit, &h->xsplit})
+                      &h->utab, &h->wsplit, &h->xsplit, &h->wt64})
         b->release();
     if (h->W) cudaFree(h->W);
     for (int p = 0; p < kMaxRanks; ++p)
@@ -279,7 +288,7 @@ som_status som_set_stream(som_ctx* h, void* cuda_stream) {
 som_status som_set_weights(som_ctx* h, const float* w) {
     CHECK_HANDLE(h);
     if (!w) return fail(SOM_EINVAL, "null weights");
-    h->w_split_valid = false;
+    invalidate_w_caches(h);
     const size_t rowb = sizeof(float) * (size_t)h->dim;
     CK(cudaMemcpy2DAsync(h->W, rowb, w + (size_t)h->rank * h->dim, rowb * h->world, rowb, (size_t)h->NL,
                          cudaMemcpyDefault, h->stream));
@@ -302,7 +311,7 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     if (!X) return fail(SOM_EINVAL, "null X");
     if (n < 1) return fail(SOM_EEMPTY, "n = 0");
     const int N = h->N;
-    h->w_split_valid = false;
+    invalidate_w_caches(h);
     std::vector<int64_t> idx((size_t)N);
     if (N <= n) {
         // Floyd's sampling without replacement, draws from SplitMix64(seed)
@@ -344,6 +353,7 @@ struct CsrIn {
     const int32_t* col;
     const float* val;
     int maxnnz;
+    int64_t nnz;
 };
 
 // shared argument checks of som_train_online / som_train_online_csr; on OK
@@ -435,6 +445,7 @@ som_status stage_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, cons
     out->col = (const int32_t*)cd;
     out->val = (const float*)vd;
     out->maxnnz = res[1];
+    out->nnz = nnz;
     return SOM_OK;
 }
 
@@ -476,7 +487,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
                       double sigma0, const som_schedule& sd, uint64_t seed, int64_t t_begin, int64_t t_end,
                       int32_t* bmu_log) {
     const int64_t T = (int64_t)epochs * n;
-    h->w_split_valid = false;
+    invalidate_w_caches(h);
     som_status st = SOM_OK;
     if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
 
@@ -679,7 +690,7 @@ som_status som_comm_init(som_ctx* h, int32_t rank, int32_t world) {
     h->world = world;
     h->NL = NL;
     h->peer_mail[rank] = h->mail;
-    h->w_split_valid = false;
+    invalidate_w_caches(h);
     return SOM_OK;
 }
 
@@ -764,7 +775,7 @@ som_status som_last_train_config(som_ctx* h, int32_t* grid, int32_t* kernel) {
 
 som_status som_set_map_precision(som_ctx* h, int32_t precision) {
     CHECK_HANDLE(h);
-    if (precision < SOM_MAP_AUTO || precision > SOM_MAP_3XTF32) return fail(SOM_EINVAL, "unknown map precision");
+    if (precision < SOM_MAP_AUTO || precision > SOM_MAP_SPARSE_F64) return fail(SOM_EINVAL, "unknown map precision");
     h->map_precision = precision;
     return SOM_OK;
 }
@@ -774,7 +785,7 @@ namespace {
 // Which mapping path serves a call (som_set_map_precision; AUTO picks the
 // tensor cores once the contraction is large enough to amortise the split).
 bool use_tc(const som_ctx* h, int64_t n) {
-    if (h->map_precision == SOM_MAP_EXACT_F64) return false;
+    if (h->map_precision == SOM_MAP_EXACT_F64 || h->map_precision == SOM_MAP_SPARSE_F64) return false;
     if (h->map_precision == SOM_MAP_3XTF32) return true;
     return (double)n * h->N * h->dim >= 1.0e10;
 }
@@ -825,6 +836,9 @@ som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, int32_t* b1
     return SOM_OK;
 }
 
+som_status map_exact_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2,
+                         int* launches);
+
 // Map n rows of the device matrix Xd into device outputs (all device).
 som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches) {
     if (use_tc(h, n)) {
@@ -833,6 +847,12 @@ som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, in
         };
         return map_tc_rows(h, n, fill, b1, b2, d2, launches);
     }
+    return map_exact_dev(h, Xd, n, b1, b2, d2, launches);
+}
+
+// Exact dense definition (R10) of n device rows.
+som_status map_exact_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2,
+                         int* launches) {
     const int tiles_m = map_exact_tiles_m(n);
     const int tiles_n = map_exact_tiles_n(h->N);
     int nsplit = std::max(1, std::min(tiles_n, (2 * h->sm_count + tiles_m - 1) / tiles_m));
@@ -866,6 +886,121 @@ som_status copy_back(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float*
     if (o.host1) CK(cudaMemcpyAsync(bmu1, o.b1, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
     if (o.host2) CK(cudaMemcpyAsync(bmu2, o.b2, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
     if (o.host3) CK(cudaMemcpyAsync(d2, o.d2, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+    return SOM_OK;
+}
+
+// W^T (fp64 or fp32) and |w|^2 for the sparse path (map_sparse.cu), cached until W changes.
+som_status ensure_wt(som_ctx* h, int J, bool f32, const void** WT, const double** wsq, int* Np, bool* fresh) {
+    const int np = sparse_padded_units(h->N, J);
+    const size_t plane = (f32 ? sizeof(float) : sizeof(double)) * (size_t)h->dim * np;
+    *fresh = !h->wt_valid || h->wt_J != J || h->wt_f32 != f32;
+    if (*fresh) {
+        CK(h->wt64.ensure(plane + sizeof(double) * (size_t)h->N, h->stream));
+        char* base = (char*)h->wt64.p;
+        CK(launch_wt(h->W, h->N, h->dim, np, f32, base, (double*)(base + plane), h->stream));
+        h->wt_valid = true;
+        h->wt_J = J;
+        h->wt_f32 = f32;
+    }
+    *WT = h->wt64.p;
+    *wsq = (const double*)((const char*)h->wt64.p + plane);
+    *Np = np;
+    return SOM_OK;
+}
+
+// Sparse kernel configuration: tile = 64 J units, W^T storage fp32 or fp64
+// (SOM_SPARSE_J / SOM_SPARSE_F32 override, for tuning).
+void sparse_cfg(const som_ctx* h, int* J, bool* f32) {
+    *f32 = true;
+    *J = h->N >= 2048 ? 8 : (h->N >= 512 ? 4 : 2);
+    if (const char* e = std::getenv("SOM_SPARSE_F32")) *f32 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SOM_SPARSE_J")) {
+        const int j = std::atoi(e);
+        if (j == 1 || j == 2 || j == 4 || j == 8) *J = j;
+    }
+    if (*f32 && *J == 1) *J = 2;
+    if (!*f32 && *J == 8) *J = 4;
+}
+
+// Which path maps CSR rows: the exact sparse identity (R25) unless the
+// caller forces another precision, or AUTO finds the dense contraction
+// cheaper (rows with more than ~1.5 % of the terms set).
+int csr_path(const som_ctx* h, const CsrIn& csr, int64_t n) {
+    if (h->map_precision != SOM_MAP_AUTO) return h->map_precision;
+    const double avg_nnz = (double)csr.nnz / (double)n;
+    if (avg_nnz <= 0.015 * h->dim) return SOM_MAP_SPARSE_F64;
+    return use_tc(h, n) ? SOM_MAP_3XTF32 : SOM_MAP_EXACT_F64;
+}
+
+// Map n staged CSR rows into device outputs.
+som_status map_csr_dev(som_ctx* h, const CsrIn& csr, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches) {
+    const int path = csr_path(h, csr, n);
+    if (path == SOM_MAP_SPARSE_F64) {
+        int J = 4;
+        bool f32 = true, fresh = false;
+        sparse_cfg(h, &J, &f32);
+        const void* WT;
+        const double* wsq;
+        int np = 0;
+        som_status st = ensure_wt(h, J, f32, &WT, &wsq, &np, &fresh);
+        if (st) return st;
+        if (fresh) *launches += 2;
+        const int tiles = np / sparse_tile_units(J);
+        // chunk so the partial keys stay <= 1 GiB
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, ((int64_t)1 << 30) / (16 * (int64_t)tiles)));
+        CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles * (size_t)chunk, h->stream));
+        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+            const int64_t m = std::min(chunk, n - r0);
+            CK(launch_map_sparse(csr.rowptr, csr.col, csr.val, r0, m, WT, f32, wsq, h->N, np, J,
+                                 (unsigned long long*)h->keys.p, h->stream));
+            CK(launch_map_merge((const unsigned long long*)h->keys.p, tiles, m, b1 + r0, b2 ? b2 + r0 : nullptr,
+                                d2 ? d2 + r0 : nullptr, h->stream));
+            *launches += 2;
+        }
+        return SOM_OK;
+    }
+    if (path == SOM_MAP_3XTF32) {
+        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
+            return launch_split_csr(csr.rowptr, csr.col, csr.val, r0, m, h->dim, hi, lo, nrm, h->stream);
+        };
+        return map_tc_rows(h, n, fill, b1, b2, d2, launches);
+    }
+    // exact dense definition: densify in chunks of <= 1 GiB and map each chunk
+    const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));
+    CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim, h->stream));
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t m = std::min(chunk, n - r0);
+        CK(launch_densify(csr.rowptr, csr.col, csr.val, r0, m, h->dim, (float*)h->dense.p, h->stream));
+        ++*launches;
+        som_status st = map_exact_dev(h, (const float*)h->dense.p, m, b1 + r0, b2 ? b2 + r0 : nullptr,
+                                      d2 ? d2 + r0 : nullptr, launches);
+        if (st) return st;
+    }
+    return SOM_OK;
+}
+
+// QE/TE sums from device mapping outputs (deterministic two-pass), then
+// the call's timing; ev0 was recorded before the mapping.
+som_status finish_errors(som_ctx* h, int64_t n, const OutStage& o, int launches, double* qe, double* te) {
+    const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
+    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2), h->stream));
+    double* partial = (double*)h->red.p;
+    unsigned long long* pcnt = (unsigned long long*)(partial + nb);
+    double* osum = (double*)(pcnt + nb);
+    unsigned long long* obad = (unsigned long long*)(osum + 1);
+    CK(launch_errors(o.b1, o.b2, o.d2, n, h->rows, h->cols, h->topo, partial, pcnt, nb, osum, obad, h->stream));
+    launches += 2;
+    CK(cudaEventRecord(h->ev1, h->stream));
+    double sum = 0;
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&sum, osum, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(&bad, obad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (qe) *qe = sum / (double)n;
+    if (te) *te = (double)bad / (double)n;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = n; h->last_launches = launches;
     return SOM_OK;
 }
 
@@ -906,41 +1041,11 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
     CsrIn csr{};
     som_status st = stage_csr(h, rowptr, col, val, n, &csr);
     if (st) return st;
-    const void* rpd = csr.rowptr;
-    const void* cd = csr.col;
-    const void* vd = csr.val;
     OutStage o;
     if ((st = stage_outputs(h, n, bmu1, bmu2, d2, false, o))) return st;
-    if (use_tc(h, n)) {
-        int launches = 0;
-        CK(cudaEventRecord(h->ev0, h->stream));
-        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
-            return launch_split_csr((const int64_t*)rpd, (const int32_t*)cd, (const float*)vd, r0, m, h->dim, hi, lo,
-                                    nrm, h->stream);
-        };
-        if ((st = map_tc_rows(h, n, fill, o.b1, o.b2, o.d2, &launches))) return st;
-        CK(cudaEventRecord(h->ev1, h->stream));
-        if ((st = copy_back(h, n, bmu1, bmu2, d2, o))) return st;
-        CK(cudaStreamSynchronize(h->stream));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-        h->last_ms = ms; h->last_units = n; h->last_launches = launches;
-        return SOM_OK;
-    }
-    // densify in chunks of <= 1 GiB and map each chunk
-    const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));
-    CK(h->dense.ensure(sizeof(float) * (size_t)chunk * h->dim, h->stream));
     int launches = 0;
     CK(cudaEventRecord(h->ev0, h->stream));
-    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
-        const int64_t m = std::min(chunk, n - r0);
-        CK(launch_densify((const int64_t*)rpd, (const int32_t*)cd, (const float*)vd, r0, m, h->dim, (float*)h->dense.p,
-                          h->stream));
-        ++launches;
-        if ((st = map_dense_dev(h, (const float*)h->dense.p, m, o.b1 + r0, o.b2 ? o.b2 + r0 : nullptr,
-                                o.d2 ? o.d2 + r0 : nullptr, &launches)))
-            return st;
-    }
+    if ((st = map_csr_dev(h, csr, n, o.b1, o.b2, o.d2, &launches))) return st;
     CK(cudaEventRecord(h->ev1, h->stream));
     if ((st = copy_back(h, n, bmu1, bmu2, d2, o))) return st;
     CK(cudaStreamSynchronize(h->stream));
@@ -948,6 +1053,23 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_ms = ms; h->last_units = n; h->last_launches = launches;
     return SOM_OK;
+}
+
+som_status som_errors_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                          double* qe, double* te) {
+    CHECK_HANDLE(h);
+    if (h->world > 1)
+        return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    CsrIn csr{};
+    som_status st = stage_csr(h, rowptr, col, val, n, &csr);
+    if (st) return st;
+    OutStage o;
+    if ((st = stage_outputs(h, n, nullptr, nullptr, nullptr, true, o))) return st;
+    int launches = 0;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if ((st = map_csr_dev(h, csr, n, o.b1, o.b2, o.d2, &launches))) return st;
+    return finish_errors(h, n, o, launches, qe, te);
 }
 
 som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double* te) {
@@ -964,26 +1086,7 @@ som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double*
     int launches = 0;
     CK(cudaEventRecord(h->ev0, h->stream));
     if ((st = map_dense_dev(h, (const float*)Xd, n, o.b1, o.b2, o.d2, &launches))) return st;
-    const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
-    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2), h->stream));
-    double* partial = (double*)h->red.p;
-    unsigned long long* pcnt = (unsigned long long*)(partial + nb);
-    double* osum = (double*)(pcnt + nb);
-    unsigned long long* obad = (unsigned long long*)(osum + 1);
-    CK(launch_errors(o.b1, o.b2, o.d2, n, h->rows, h->cols, h->topo, partial, pcnt, nb, osum, obad, h->stream));
-    launches += 2;
-    CK(cudaEventRecord(h->ev1, h->stream));
-    double sum = 0;
-    unsigned long long bad = 0;
-    CK(cudaMemcpyAsync(&sum, osum, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(&bad, obad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (qe) *qe = sum / (double)n;
-    if (te) *te = (double)bad / (double)n;
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-    h->last_ms = ms; h->last_units = n; h->last_launches = launches;
-    return SOM_OK;
+    return finish_errors(h, n, o, launches, qe, te);
 }
 
 som_status som_qerror(som_ctx* h, const float* X, int64_t n, double* qe) {

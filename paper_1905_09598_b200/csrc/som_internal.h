@@ -193,6 +193,18 @@ cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm
                           const float* wlo, const float* wnorm, int N, int d, unsigned long long* keys, int sm_count,
                           cudaStream_t st);
 
+// Exact sparse mapping (map_sparse.cu, R25): W^T (dim x Np, Np = N padded
+// to the 64 J-unit tile; fp64, or fp32 widened exactly in registers) +
+// |w|^2 fp64; partial top-2 keys [Np / (64 J)][m][2] per chunk of m CSR
+// rows starting at r0, merged by launch_map_merge.  (J, f32) in
+// {1,2,4} x fp64, {2,4,8} x fp32.
+int sparse_tile_units(int J);
+int sparse_padded_units(int N, int J);
+cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, double* wsq, cudaStream_t st);
+cudaError_t launch_map_sparse(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t m,
+                              const void* WT, bool f32, const double* wsq, int N, int Np, int J,
+                              unsigned long long* keys, cudaStream_t st);
+
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libsom.so")
 SOM_OK, SOM_EINVAL, SOM_EDIM, SOM_EEMPTY, SOM_ENOMEM, SOM_ECUDA, SOM_ENCCL, SOM_ESTATE, SOM_EUNSUPPORTED = range(9)
 SOM_RECT, SOM_HEX = 0, 1
 SOM_DECAY_GAUSSIAN, SOM_DECAY_LINEAR, SOM_DECAY_EXP = 0, 1, 2
-SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32 = 0, 1, 2
+SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32, SOM_MAP_SPARSE_F64 = 0, 1, 2, 3
 SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL, SOM_TRAIN_W_REGISTERS = 0, 1, 2, 3
 
 _STATUS = {0: "SOM_OK", 1: "SOM_EINVAL", 2: "SOM_EDIM", 3: "SOM_EEMPTY", 4: "SOM_ENOMEM", 5: "SOM_ECUDA",
@@ -43,7 +43,7 @@ _lib = None
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
            "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
-           "som_qerror", "som_topographic_error", "som_errors", "som_umatrix", "som_set_stream",
+           "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
            "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
 
@@ -75,6 +75,7 @@ def lib():
         "som_qerror": [P, P, i64, P],
         "som_topographic_error": [P, P, i64, P],
         "som_errors": [P, P, i64, P, P],
+        "som_errors_csr": [P, P, P, P, i64, P, P],
         "som_umatrix": [P, P],
         "som_set_stream": [P, P],
         "som_last_stats": [P, P, P, P],
@@ -222,6 +223,13 @@ def som_errors(h, X, n: int) -> tuple[float, float]:
     return q.value, t.value
 
 
+def som_errors_csr(h, rowptr, col, val, n: int) -> tuple[float, float]:
+    q, t = ctypes.c_double(), ctypes.c_double()
+    _check(lib().som_errors_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                                ctypes.byref(q), ctypes.byref(t)))
+    return q.value, t.value
+
+
 def som_umatrix(h, U) -> None:
     _check(lib().som_umatrix(h, _ptr(U, np.float32, True)))
 
@@ -344,8 +352,21 @@ class SOM:
         som_map(self.h, X, n, b1, b2, d2)
         return b1, b2, d2
 
+    def map_csr(self, rowptr, col, val, n: int, want_bmu2: bool = True, want_d2: bool = True):
+        b1 = np.empty(n, np.int32)
+        b2 = np.empty(n, np.int32) if want_bmu2 else None
+        d2 = np.empty(n, np.float32) if want_d2 else None
+        som_map_csr(self.h, rowptr, col, val, n, b1, b2, d2)
+        return b1, b2, d2
+
     def errors(self, X):
         return som_errors(self.h, X, X.shape[0])
+
+    def errors_csr(self, rowptr, col, val, n: int):
+        return som_errors_csr(self.h, rowptr, col, val, n)
+
+    def set_map_precision(self, precision: int):
+        som_set_map_precision(self.h, precision)
 
     def umatrix(self):
         U = np.empty(self.N, np.float32)

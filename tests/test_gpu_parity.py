@@ -174,6 +174,7 @@ def test_map_csr_matches_dense(som):
     with som.SOM(10, 15, 2000, 1) as m:
         m.set_weights(W0)
         a = m.map(X)
+        som.som_set_map_precision(m.h, som.SOM_MAP_EXACT_F64)   # densified CSR through the exact path
         b1 = np.empty(C.n, np.int32)
         b2 = np.empty(C.n, np.int32)
         d1 = np.empty(C.n, np.float32)
