@@ -22,6 +22,11 @@ WANT = [
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe % (active)"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("smsp__average_warp_latency_issue_stalled_barrier", "stall barrier"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2 -> L1 bytes"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait / issue"),
+    ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "stall mio_throttle / issue"),
 ]
 
 
