@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--map-docs", type=int, default=200000, help="documents in the c5-shaped mapping leg (0 = skip)")
     p.add_argument("--c3-steps", type=int, default=20000, help="steps of the c3 training leg (0 = skip)")
+    p.add_argument("--table3-steps", type=int, default=20000, help="steps per map of the Table 3 leg (0 = skip)")
     return p.parse_args()
 
 
@@ -244,6 +245,39 @@ def updated_units(rows, cols, topo, bmu_log, t0, T, sigma0, eps=1e-4, k=math.log
     return out
 
 
+TABLE3_PAPER_S = {16: 34.25, 32: 32.81, 64: 33.37, 128: 38.40, 256: 111.03, 512: 431.38}
+
+
+def table3_leg(som, torch, args, local, seed):
+    """The paper's map-size study (Table 3): online training with
+    weight length 64 on square hex maps 16x16 ... 512x512, same data (10,000
+    uniform rows) and the same number of steps for every map; kernel time
+    per map and the ratio per doubling beside the paper's ratios."""
+    from synth import uniform_matrix
+    n, d, steps = 10000, 64, args.table3_steps
+    X = torch.from_numpy(uniform_matrix(n, d, seed + 64)).cuda(local)
+    rows, prev = [], None
+    for side in (16, 32, 64, 128, 256, 512):
+        W0 = torch.from_numpy(uniform_matrix(side * side, d, seed + side)).cuda(local)
+        with som.SOM(side, side, d, 1, device=local) as m:
+            som.som_set_stream(m.h, torch.cuda.current_stream())
+            epochs = (steps + n - 1) // n
+            m.set_weights(W0)
+            som.som_train_online(m.h, X, n, epochs, ALPHA0, side / 2.0, None, seed, 0, min(steps, 500), None)
+            m.set_weights(W0)
+            som.som_train_online(m.h, X, n, epochs, ALPHA0, side / 2.0, None, seed, 0, steps, None)
+            ms, units, _ = som.som_last_stats(m.h)
+            g, k = som.som_last_train_config(m.h)
+        rows.append({"map": f"{side}x{side}", "us_per_step": 1000.0 * ms / units, "samples_per_s": units / (ms / 1e3),
+                     "ratio": None if prev is None else ms / prev,
+                     "paper_ratio": None if side == 16 else TABLE3_PAPER_S[side] / TABLE3_PAPER_S[side // 2],
+                     "grid": g})
+        prev = ms
+    return {"workload": f"Table 3 study: d = 64, hex maps 16^2..512^2, {n} uniform rows, {steps} steps each "
+                        "(short-row kernel train_small.cu)", "maps": rows,
+            "paper": "CUDASOM on a Quadro P5000, seconds: " + ", ".join(f"{k}^2 {v}" for k, v in TABLE3_PAPER_S.items())}
+
+
 def train_c3_leg(som, torch, args, local, seed):
     """Online training in the bandwidth-bound regime: c3 (50x50 hex, 50k x 10k,
     W = 100 MB streamed through L2/HBM every step), first `--c3-steps` steps."""
@@ -432,6 +466,7 @@ def run_b200(args, rank, world, local):
              2: "som_train_reg_kernel (W registers)"}.get(k_used, "?")
     mapping = mapping_leg(som, torch, args, local, seed) if args.map_docs > 0 else None
     train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
+    table3 = table3_leg(som, torch, args, local, seed) if args.table3_steps > 0 else None
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -468,6 +503,7 @@ def run_b200(args, rank, world, local):
         "gpu_launches": launches,
         "mapping": mapping,
         "train_c3": train_c3,
+        "table3": table3,
         "roofline": {"bound": "alu", "kernel": f"{kname}, G={g_used}", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,

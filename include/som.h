@@ -138,10 +138,15 @@ som_status som_train_online_csr(som_ctx *h, const int64_t *rowptr, const int32_t
 /* Where som_train_online keeps each CTA's prototypes between steps:
  * AUTO picks shared memory when a CTA's share of W fits (else global
  * memory, L2-resident when W fits the L2); REGISTERS keeps each CTA's share
- * in registers (small maps, d % 4 == 0).  Forcing a placement that does not
- * fit returns SOM_EUNSUPPORTED from som_train_online. */
+ * in registers (small maps, d % 4 == 0); SHORT_ROWS is the kernel for short
+ * prototypes (d <= 128, d % 4 == 0; Table 3's d = 64): one group of
+ * d/4 lanes per unit, W in registers or streamed from L2, neighbourhood
+ * from separable tables (R26).  AUTO picks SHORT_ROWS whenever it applies.
+ * Forcing a placement that does not fit returns SOM_EUNSUPPORTED from
+ * som_train_online. */
 typedef enum {
-    SOM_TRAIN_AUTO = 0, SOM_TRAIN_W_SHARED = 1, SOM_TRAIN_W_GLOBAL = 2, SOM_TRAIN_W_REGISTERS = 3
+    SOM_TRAIN_AUTO = 0, SOM_TRAIN_W_SHARED = 1, SOM_TRAIN_W_GLOBAL = 2, SOM_TRAIN_W_REGISTERS = 3,
+    SOM_TRAIN_SHORT_ROWS = 4
 } som_train_mode;
 som_status som_set_train_mode(som_ctx *h, int32_t mode);
 
@@ -153,7 +158,8 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
 /* Grid and kernel variant of the last som_train_online call:
  * kernel 0 = W in global memory (generic), 1 = W in shared memory,
  * 2 = W in registers, 3 = W in global memory (pipelined, d % 4 == 0),
- * 4 = W in global memory with the sparse distance path (CSR input). */
+ * 4 = W in global memory with the sparse distance path (CSR input),
+ * 5 = short-row kernel (SOM_TRAIN_SHORT_ROWS). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* ---- Neuron sharding: online training of one map across

@@ -505,8 +505,31 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // the register file: G minimises (all-gather latency + fp64 distance
     // time), both measured on B200 (profiles/probe_*_r01.json).  Otherwise
     // one persistent CTA per SM with W in shared or global memory.
+    // short prototypes (d <= 128): the lane-group kernel (train_small.cu).
+    // G minimises (all-gather latency + per-CTA rounds of work), with the
+    // L2 traffic of the streamed variant when the map exceeds 4 rounds.
+    bool use_small = false;
+    if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_SHORT_ROWS) && a.x_vec4 &&
+        train_small_supported(h->dim)) {
+        auto xchg_us = [](int G) { return G <= 32 ? 0.65 : G <= 64 ? 0.70 : G <= 128 ? 0.85 : 1.65; };
+        const int gmax = std::min(h->NL, h->sm_count);
+        double best = 1e30;
+        int bestG = 0;
+        for (int G : {8, 16, 32, 64, 128, gmax}) {
+            if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
+            if (G < 1 || G > gmax) continue;
+            const int R = small_rounds((h->NL + G - 1) / G, h->dim);
+            double est = xchg_us(G) + 0.1 * R;
+            if (R > 4) est += 2.6 * 4.0 * (double)h->NL * h->dim / 12.0e6;   // read + ~60 % written, 12 TB/s L2
+            if (est < best) { best = est; bestG = G; }
+        }
+        use_small = bestG > 0;
+        a.G = bestG;
+    }
+    if (h->train_mode == SOM_TRAIN_SHORT_ROWS && !use_small)
+        return fail(SOM_EUNSUPPORTED, "short-row kernel needs d <= 128 and d %% 4 == 0");
     bool use_reg = false;
-    if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
+    if (!use_small && (h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
         // all-gather latency by grid size (profiles/probe_xchg_r01.json) and
         // per-CTA F2F-bound distance time: (S + 1) * d conversions at 16/clk
         // (power-of-two grids measured fastest: 16-64 ~0.6-0.7 us, 128 ~0.8 us,
@@ -529,7 +552,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     }
     if (h->train_mode == SOM_TRAIN_W_REGISTERS && !use_reg)
         return fail(SOM_EUNSUPPORTED, "map share per CTA does not fit registers (or d %% 4 != 0)");
-    if (!use_reg) {
+    if (!use_reg && !use_small) {
         a.G = std::min(h->NL, h->sm_count);
         if (h->train_grid > 0) a.G = std::min(a.G, h->train_grid);
     }
@@ -549,15 +572,20 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     if (!a.w_smem) smem = train_smem_bytes(a.S, a.dimp, 0);
     // maps that do not fit on chip stream from global memory with the
     // pipelined kernel (train_glb.cu) when its layout applies
-    const bool use_glb = !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
+    const bool use_glb = !use_small && !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
     if (use_reg) smem = sizeof(float) * (3 * (size_t)a.dimp + (size_t)a.rows * (a.topo == 0 ? a.cols : 2 * a.cols));
     if (use_glb) smem = sizeof(float) * 2 * (size_t)a.dimp;
+    if (use_small) {
+        a.w_smem = 0;
+        smem = sizeof(float) * 3 * (size_t)a.dimp +
+               sizeof(double) * ((size_t)a.dimp + a.rows + (a.topo == 0 ? a.cols : 2 * a.cols));
+    }
     // CSR input: the sparse-distance kernel where W streams from global
     // memory; on-chip maps (latency-bound, no gain) and layouts it does not
     // cover train on the densified rows
     bool use_csr = false;
     if (csr) {
-        use_csr = !use_reg && !a.w_smem && train_csr_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin);
+        use_csr = !use_small && !use_reg && !a.w_smem && train_csr_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin);
         if (use_csr) {
             a.rowptr = csr->rowptr; a.col = csr->col; a.val = csr->val;
             a.nz_cap = csr_nz_cap(csr->maxnnz);
@@ -599,7 +627,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // persisting access-policy window (random X rows stream past it), undone
     // after the launch so the caller's stream is left as it was.
     bool l2_window = false;
-    if (!use_reg && !a.w_smem) {
+    if (!use_reg && !a.w_smem && (!use_small || small_rounds(a.S, h->dim) > 4)) {
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
@@ -620,7 +648,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         }
     }
     CK(cudaEventRecord(h->ev0, h->stream));
-    if (use_reg) CK(launch_train_reg(a, h->stream));
+    if (use_small) CK(launch_train_small(a, h->stream));
+    else if (use_reg) CK(launch_train_reg(a, h->stream));
     else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
@@ -633,7 +662,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -745,7 +774,7 @@ som_status som_comm_mailbox_ptr(som_ctx* h, void** mailbox) {
 
 som_status som_set_train_mode(som_ctx* h, int32_t mode) {
     CHECK_HANDLE(h);
-    if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_W_REGISTERS) return fail(SOM_EINVAL, "unknown train mode");
+    if (mode < SOM_TRAIN_AUTO || mode > SOM_TRAIN_SHORT_ROWS) return fail(SOM_EINVAL, "unknown train mode");
     h->train_mode = mode;
     return SOM_OK;
 }

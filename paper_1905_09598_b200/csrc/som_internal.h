@@ -158,6 +158,14 @@ cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st);
 bool train_glb_supported(int S, int dim);
 cudaError_t launch_train_glb(const TrainArgs& a, cudaStream_t st);
 
+// short-prototype variant (train_small.cu): d <= 128, d % 4 == 0; a group
+// of small_lanes(d) lanes per unit (4 float4 per lane); W in registers for
+// up to 4 rounds of 16*32/L units per CTA, else streamed from global memory
+bool train_small_supported(int dim);
+int small_lanes(int dim);
+int small_rounds(int S, int dim);
+cudaError_t launch_train_small(const TrainArgs& a, cudaStream_t st);
+
 // CSR-input variant with the sparse distance path (train_csr.cu)
 int csr_nz_cap(int maxnnz);
 bool train_csr_supported(int S, int dim, int maxnnz, int max_smem_optin);
