@@ -63,6 +63,8 @@ def lib():
         L.or_map.argtypes = [P, i64, i64, P, i64, P, P, P, P, P]
         L.or_map_csr.restype = None
         L.or_map_csr.argtypes = [P, P, i64, i64, P, P, P, i64, P, P, P, P, P]
+        L.or_train_batch.restype = ctypes.c_int
+        L.or_train_batch.argtypes = [P, i32, i32, i32, i64, P, i64, i32, f64, i32, f64, f64, f64, P]
         L.or_row_sqnorm.restype = None
         L.or_row_sqnorm.argtypes = [P, i64, i64, P]
         L.or_qerror_from_d1.restype = f64
@@ -147,6 +149,20 @@ def train_online(W, rows, cols, topo, X, epochs, alpha0, sigma0, seed,
 
 
 # --------------------------------------------------------------- mapping
+def train_batch(W, rows, cols, topo, X, epochs, sigma0, kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0,
+                eps=1e-4):
+    """Batch SOM (R27) on a copy of W.  Returns (W', BMUs after the last epoch)."""
+    W = np.array(W, dtype=np.float32, copy=True, order="C")
+    X = _f32(X)
+    n, d = X.shape
+    assert W.shape == (rows * cols, d)
+    b = np.empty(n, np.int32)
+    r = lib().or_train_batch(_p(W), rows, cols, topo, d, _p(X), n, epochs, sigma0, kind, k, sigma_min, eps, _p(b))
+    if r != 0:
+        raise ValueError("or_train_batch: bad arguments")
+    return W, b
+
+
 def map_docs(W, X, want_margins=False):
     W, X = _f32(W), _f32(X)
     N, d = W.shape

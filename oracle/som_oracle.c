@@ -279,6 +279,62 @@ void or_map_csr(const float *W, const double *wsq, int64_t N, int64_t d,
     }
 }
 
+/* ------------------------------------------------------------ batch SOM */
+/* Batch SOM (the variant of [25], [26], and
+ * "most of the recent proposals have focused on the batch version of SOM",
+ * P:158).  The paper does not state it; reading R27 takes Kohonen's batch
+ * map: per epoch e in [0, E), with the current W,
+ *   c_i  = BMU of x_i (R9, R10, every document),
+ *   h_iu = exp(-g2(c_i, u) / (2 sigma_e^2)) if g2 <= r2_e else 0   (R4, R5
+ *          without the learning rate: the batch map has none),
+ *   W_u  <- RN_fp32( sum_i h_iu x_i / sum_i h_iu )   if sum_i h_iu > 0,
+ *          else W_u unchanged,
+ * with sigma_e, r2_e from the decay schedule at tau = e/E (R1-R3, R5).
+ * Sums run over documents in index order in fp64, straight from the
+ * definition (no per-BMU regrouping).  bmu_last (nullable, n) receives the
+ * BMUs of the final epoch.  Returns 0, or -1 on bad arguments. */
+int or_train_batch(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t d,
+                   const float *X, int64_t n, int32_t epochs, double sigma0,
+                   int32_t decay_kind, double k, double sigma_min, double eps,
+                   int32_t *bmu_last)
+{
+    if (n < 1 || epochs < 0) return -1;
+    int64_t N = (int64_t)rows * cols;
+    int64_t *c = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    float *Wn = (float *)malloc(sizeof(float) * (size_t)(N * d));
+    if (!c || !Wn) { free(c); free(Wn); return -1; }
+    for (int32_t e = 0; e < epochs; ++e) {
+        double alpha, sigma, r2;
+        or_schedule(decay_kind, k, e, epochs, 1.0, sigma0, sigma_min, eps, &alpha, &sigma, &r2);
+        (void)alpha;
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int64_t i = 0; i < n; ++i) c[i] = or_bmu(W, N, d, X + i * d, NULL, NULL);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t u = 0; u < N; ++u) {
+            double den = 0.0;
+            double *num = (double *)calloc((size_t)d, sizeof(double));
+            for (int64_t i = 0; i < n; ++i) {
+                double g2 = or_lattice_g2(rows, cols, topo, u, c[i]);
+                if (!(g2 <= r2)) continue;
+                double h = exp(-g2 / (2.0 * sigma * sigma));
+                den += h;
+                const float *x = X + i * d;
+                for (int64_t kk = 0; kk < d; ++kk) num[kk] += h * (double)x[kk];
+            }
+            for (int64_t kk = 0; kk < d; ++kk)
+                Wn[u * d + kk] = (den > 0.0) ? (float)(num[kk] / den) : W[u * d + kk];
+            free(num);
+        }
+        memcpy(W, Wn, sizeof(float) * (size_t)(N * d));
+    }
+    if (bmu_last) {
+        for (int64_t i = 0; i < n; ++i) bmu_last[i] = (int32_t)or_bmu(W, N, d, X + i * d, NULL, NULL);
+    }
+    free(c);
+    free(Wn);
+    return 0;
+}
+
 /* fp64 squared norms of the prototypes (input to or_map_csr). */
 void or_row_sqnorm(const float *W, int64_t N, int64_t d, double *wsq)
 {

@@ -317,3 +317,69 @@ def test_qe_improves_on_bank_corpus():
     q0 = oracle.qerror(W0, X)
     Wf, _ = oracle.train_online(W0, 10, 10, 0, X, epochs=10, alpha0=0.1, sigma0=5.0, seed=1)
     assert oracle.qerror(Wf, X) <= 0.8 * q0
+
+
+# ------------------------------------------------------------ batch SOM (R27)
+def _f32(v):
+    return struct.unpack("f", struct.pack("f", float(v)))[0]
+
+
+def test_batch_closed_form_two_units():
+    """1x2 map, two documents, one epoch, no cutoff: each document's BMU is
+    the unit it sits next to, h = 1 at distance 0 and q = exp(-1/(2 sigma0^2))
+    between the units (tau = 0, f = 1, floor sigma_min below sigma0), so
+        W0' = (x1 + q x2) / (1 + q),  W1' = (q x1 + x2) / (q + 1),
+    evaluated here in exact rational arithmetic from the fp64 q and rounded
+    once to fp32."""
+    sigma0 = 0.8
+    x1 = np.array([0.125, 0.75, 0.3], np.float32)
+    x2 = np.array([0.9, 0.0625, 0.55], np.float32)
+    W0 = np.stack([x1 + np.float32(0.01), x2 - np.float32(0.01)]).astype(np.float32)
+    W, b = oracle.train_batch(W0, 1, 2, 0, np.stack([x1, x2]), 1, sigma0, sigma_min=0.1, eps=0.0)
+    q = Fraction(math.exp(-1.0 / (2.0 * sigma0 * sigma0)))
+    for k in range(3):
+        a1, a2 = Fraction(float(x1[k])), Fraction(float(x2[k]))
+        assert W[0, k] == _f32((a1 + q * a2) / (1 + q))
+        assert W[1, k] == _f32((q * a1 + a2) / (q + 1))
+    assert list(b) == [0, 1]
+
+
+def test_batch_reduces_to_kmeans_step():
+    """With a neighbourhood radius below the smallest lattice distance
+    (sigma0 = sigma_min = 0.1, eps = 1e-4: r2 = 0.18 < 1) only the BMU
+    itself gets weight, and one epoch is one Lloyd (k-means) step: every
+    unit becomes the mean of its documents, units without documents keep
+    their weights.  Checked against numpy's own argmin and mean."""
+    X = uniform_matrix(300, 7, 5).astype(np.float64)
+    W0 = uniform_matrix(12, 7, 6)
+    W0[11] += 5.0                     # far from every document: keeps its row
+    d2 = ((X[:, None, :] - W0[None, :, :].astype(np.float64)) ** 2).sum(-1)
+    srt = np.sort(d2, axis=1)
+    assert ((srt[:, 1] - srt[:, 0]) / srt[:, 0]).min() > 1e-9      # no near ties
+    c = d2.argmin(1)
+    W, _ = oracle.train_batch(W0, 3, 4, 1, X.astype(np.float32), 1, 0.1, sigma_min=0.1, eps=1e-4)
+    for u in range(12):
+        if np.any(c == u):
+            np.testing.assert_allclose(W[u], X[c == u].mean(0), rtol=0, atol=2e-7)
+        else:
+            assert np.array_equal(W[u], W0[u])
+    assert np.array_equal(W[11], W0[11])
+
+
+def test_batch_one_unit_is_the_mean_and_hull():
+    X = uniform_matrix(200, 9, 8)
+    W, b = oracle.train_batch(uniform_matrix(1, 9, 9), 1, 1, 0, X, 3, 2.0)
+    np.testing.assert_allclose(W[0], X.astype(np.float64).mean(0), rtol=0, atol=2e-7)
+    assert np.all(b == 0)
+    W2, _ = oracle.train_batch(uniform_matrix(20, 9, 10), 4, 5, 1, X, 4, 2.5, eps=0.0)
+    assert np.all(W2 >= X.min(0) - 1e-7) and np.all(W2 <= X.max(0) + 1e-7)   # weighted means
+
+
+def test_batch_fixed_point_and_zero_epochs():
+    x = uniform_matrix(1, 6, 11)
+    X = np.repeat(x, 40, axis=0)
+    W0 = uniform_matrix(9, 6, 12)
+    W, _ = oracle.train_batch(W0, 3, 3, 0, X, 1, 1.5, eps=0.0)
+    np.testing.assert_allclose(W, np.repeat(x, 9, axis=0), rtol=0, atol=1e-7)
+    W3, _ = oracle.train_batch(W0, 3, 3, 0, X, 0, 1.5)
+    assert np.array_equal(W3, W0)
