@@ -196,6 +196,21 @@ som_status som_comm_mailbox_ptr(som_ctx *h, void **mailbox);
  * NULL disables. */
 som_status som_set_trace(som_ctx *h, void *device_buf, int32_t steps);
 
+/* Batch SOM (R27: Kohonen's batch map; the variant of the
+ * GPU SOMs the paper reviews).  Per epoch e in [0, epochs),
+ * with the current W: c_i = BMU of every row (exact mapping, R10 / R25),
+ * then W_u = RN32(sum_i h(c_i,u) x_i / sum_i h(c_i,u)) where the sum is
+ * > 0 (else W_u is kept), h = exp(-g2 / 2 sigma_e^2) inside the cutoff
+ * (R4, R5, no learning rate), sigma_e from the schedule at tau = e/epochs
+ * (R1-R3).  X as in som_train_online; epochs = 0 is a no-op.  bmu
+ * (nullable, n int32, host or device) receives the BMUs under the final W.
+ * Deterministic: documents are bucketed by BMU in index order. */
+som_status som_train_batch(som_ctx *h, const float *X, int64_t n, int32_t epochs, double sigma0,
+                           const som_schedule *schedule, int32_t *bmu);
+som_status som_train_batch_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
+                               const float *val, int64_t n, int32_t epochs, double sigma0,
+                               const som_schedule *schedule, int32_t *bmu);
+
 /* Batch mapping ("assigned each document vector to the best matching
  * vector on the trained map"): for each row, bmu1 = argmin (D,u),
  * bmu2 = argmin over u != bmu1 (-1 if N = 1), d2 = D at bmu1 (squared

@@ -95,6 +95,8 @@ struct som_ctx {
     DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp32)
     DevBuf xsplit;   // tensor-core mapping: X chunk hi | lo | |x|^2
     bool w_split_valid = false;
+    DevBuf bbuf;     // batch SOM: bmu | order | scratch (int32) | cnt | off | sort temp
+    DevBuf bS, bnum; // batch SOM: per-BMU sums S and H S (fp64, N x (d+1))
     DevBuf wt64;     // sparse mapping: W^T fp64 or fp32 (dim x Np) | |W|^2 fp64 (N)
     bool wt_valid = false, wt_f32 = false;
     int wt_J = 0;
@@ -263,7 +265,7 @@ void som_destroy(som_ctx* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
-                      &h->utab, &h->wsplit, &h->xsplit, &h->wt64})
+                      &h->utab, &h->wsplit, &h->xsplit, &h->wt64, &h->bbuf, &h->bS, &h->bnum})
         b->release();
     if (h->W) cudaFree(h->W);
     for (int p = 0; p < kMaxRanks; ++p)
@@ -1082,6 +1084,109 @@ som_status som_map_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, co
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_ms = ms; h->last_units = n; h->last_launches = launches;
     return SOM_OK;
+}
+
+namespace {
+
+// Batch SOM (R27): epochs of map -> bucket -> per-BMU sums -> H S -> divide.
+som_status train_batch_impl(som_ctx* h, const float* Xd, const CsrIn* csr, int64_t n, int32_t epochs, double sigma0,
+                            const som_schedule* s, int32_t* bmu) {
+    som_schedule sd;
+    som_schedule_default(&sd);
+    if (s) sd = *s;
+    if (sd.kind < 0 || sd.kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
+    if (!(sd.k > 0.0) || !std::isfinite(sd.k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
+    if (!(sd.sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
+    if (!(sd.cutoff >= 0.0 && sd.cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
+    if (n > INT32_MAX) return fail(SOM_EUNSUPPORTED, "batch SOM: n >= 2^31 rows");
+    const int N = h->N, d = h->dim;
+    const size_t tb = batch_sort_temp_bytes(n, N);
+    const size_t ints = 4 * (size_t)n + 2 * (size_t)N;
+    CK(h->bbuf.ensure(sizeof(int32_t) * ints + tb + 256, h->stream));
+    int32_t* b = (int32_t*)h->bbuf.p;
+    int32_t* order = b + n;
+    int32_t* scratch = order + n;
+    int32_t* cnt = scratch + 2 * n;
+    int32_t* off = cnt + N;
+    void* temp = (void*)(((uintptr_t)(off + N) + 255) & ~(uintptr_t)255);
+    const size_t plane = sizeof(double) * (size_t)N * (d + 1);
+    CK(h->bS.ensure(plane, h->stream));
+    CK(h->bnum.ensure(plane, h->stream));
+    // exact BMUs: the dense definition (R10), or the sparse identity (R25) for TF-IDF-like CSR rows
+    const int saved = h->map_precision;
+    if (saved == SOM_MAP_AUTO) h->map_precision = csr ? SOM_MAP_AUTO : SOM_MAP_EXACT_F64;
+    if (csr && h->map_precision == SOM_MAP_AUTO && csr_path(h, *csr, n) == SOM_MAP_3XTF32)
+        h->map_precision = SOM_MAP_EXACT_F64;
+    auto map_all = [&](int* launches) -> som_status {
+        return csr ? map_csr_dev(h, *csr, n, b, nullptr, nullptr, launches)
+                   : map_dense_dev(h, Xd, n, b, nullptr, nullptr, launches);
+    };
+    int launches = 0;
+    som_status st = SOM_OK;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    for (int32_t e = 0; e < epochs && st == SOM_OK; ++e) {
+        // schedule at tau = e / epochs (R1-R3, R5), host fp64 as for the online decay table
+        double f = 0.0;
+        fill_decay(&f, e, e + 1, epochs, sd.kind, sd.k);
+        double sigma = sigma0 * f;
+        if (sigma < sd.sigma_min) sigma = sd.sigma_min;
+        const double r2 = sd.cutoff > 0.0 ? 2.0 * sigma * sigma * std::log(1.0 / sd.cutoff) : INFINITY;
+        if ((st = map_all(&launches))) break;
+        CK(launch_batch_bucket(b, n, N, order, cnt, off, scratch, temp, tb, h->stream));
+        if (csr) CK(launch_batch_accumulate_csr(csr->rowptr, csr->col, csr->val, d, order, off, cnt, N,
+                                                (double*)h->bS.p, h->stream));
+        else CK(launch_batch_accumulate_dense(Xd, d, order, off, cnt, N, (double*)h->bS.p, h->stream));
+        CK(launch_batch_update((const double*)h->bS.p, (double*)h->bnum.p, N, d, h->rows, h->cols, h->topo, sigma,
+                               r2, h->W, h->stream));
+        invalidate_w_caches(h);
+        launches += 7;
+    }
+    if (st == SOM_OK && bmu) {
+        st = map_all(&launches);
+        if (st == SOM_OK) {
+            if (is_device_ptr(bmu)) CK(cudaMemcpyAsync(bmu, b, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, h->stream));
+            else CK(cudaMemcpyAsync(bmu, b, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+        }
+    }
+    h->map_precision = saved;
+    if (st) return st;
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = (int64_t)epochs * n; h->last_launches = launches;
+    return SOM_OK;
+}
+
+}  // namespace
+
+som_status som_train_batch(som_ctx* h, const float* X, int64_t n, int32_t epochs, double sigma0,
+                           const som_schedule* s, int32_t* bmu) {
+    CHECK_HANDLE(h);
+    if (h->world > 1) return fail(SOM_EUNSUPPORTED, "batch SOM on a neuron-sharded handle");
+    if (!X) return fail(SOM_EINVAL, "null X");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: no data to train on");
+    if (epochs < 0) return fail(SOM_EINVAL, "epochs must be >= 0");
+    if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
+    if (epochs == 0 && !bmu) return SOM_OK;
+    const void* Xd = nullptr;
+    som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
+    if (st) return st;
+    return train_batch_impl(h, (const float*)Xd, nullptr, n, epochs, sigma0, s, bmu);
+}
+
+som_status som_train_batch_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                               int32_t epochs, double sigma0, const som_schedule* s, int32_t* bmu) {
+    CHECK_HANDLE(h);
+    if (h->world > 1) return fail(SOM_EUNSUPPORTED, "batch SOM on a neuron-sharded handle");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: no data to train on");
+    if (epochs < 0) return fail(SOM_EINVAL, "epochs must be >= 0");
+    if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
+    CsrIn csr{};
+    som_status st = stage_csr(h, rowptr, col, val, n, &csr);
+    if (st) return st;
+    if (epochs == 0 && !bmu) return SOM_OK;
+    return train_batch_impl(h, nullptr, &csr, n, epochs, sigma0, s, bmu);
 }
 
 som_status som_errors_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,

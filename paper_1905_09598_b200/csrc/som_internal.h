@@ -213,6 +213,21 @@ cudaError_t launch_map_sparse(const int64_t* rowptr, const int32_t* col, const f
                               const void* WT, bool f32, const double* wsq, int N, int Np, int J,
                               unsigned long long* keys, cudaStream_t st);
 
+// Batch SOM epoch pieces (batch.cu, R27): bucket documents by BMU (stable
+// radix sort; scratch 2 n int32), per-BMU fp64 sums S (N x (d+1), column d
+// = count), then num = H S with the separable lattice kernel and
+// W = RN32(num / den) where den > 0.
+size_t batch_sort_temp_bytes(int64_t n, int N);
+cudaError_t launch_batch_bucket(const int32_t* bmu, int64_t n, int N, int32_t* order, int32_t* cnt, int32_t* off,
+                                int32_t* scratch, void* temp, size_t temp_bytes, cudaStream_t st);
+cudaError_t launch_batch_accumulate_dense(const float* X, int d, const int32_t* order, const int32_t* off,
+                                          const int32_t* cnt, int N, double* S, cudaStream_t st);
+cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* col, const float* val, int d,
+                                        const int32_t* order, const int32_t* off, const int32_t* cnt, int N,
+                                        double* S, cudaStream_t st);
+cudaError_t launch_batch_update(const double* S, double* num, int N, int d, int rows, int cols, int topo,
+                                double sigma, double r2, float* W, cudaStream_t st);
+
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);

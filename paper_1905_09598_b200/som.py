@@ -43,6 +43,7 @@ _lib = None
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
            "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_train_batch", "som_train_batch_csr",
            "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
            "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
@@ -65,6 +66,8 @@ def lib():
         "som_init_random": [P, P, i64, u64],
         "som_train_online": [P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
         "som_train_online_csr": [P, P, P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
+        "som_train_batch": [P, P, i64, i32, f64, P, P],
+        "som_train_batch_csr": [P, P, P, P, i64, i32, f64, P, P],
         "som_map": [P, P, i64, P, P, P],
         "som_map_csr": [P, P, P, P, i64, P, P, P],
         "som_set_map_precision": [P, i32],
@@ -171,6 +174,18 @@ def som_train_online_csr(h, rowptr, col, val, n: int, epochs: int, alpha0: float
     _check(lib().som_train_online_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                                       epochs, alpha0, sigma0, sp, seed & (2**64 - 1), t_begin, t_end,
                                       _ptr(bmu_log, np.int32, writable=True)))
+
+
+def som_train_batch(h, X, n: int, epochs: int, sigma0: float, sched: som_schedule | None = None, bmu=None) -> None:
+    _check(lib().som_train_batch(h, _ptr(X, np.float32), n, epochs, sigma0,
+                                 ctypes.byref(sched) if sched is not None else None, _ptr(bmu, np.int32, True)))
+
+
+def som_train_batch_csr(h, rowptr, col, val, n: int, epochs: int, sigma0: float, sched: som_schedule | None = None,
+                        bmu=None) -> None:
+    _check(lib().som_train_batch_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                                     epochs, sigma0, ctypes.byref(sched) if sched is not None else None,
+                                     _ptr(bmu, np.int32, True)))
 
 
 def som_map(h, X, n: int, bmu1, bmu2=None, d2=None) -> None:
@@ -351,6 +366,23 @@ class SOM:
         d2 = np.empty(n, np.float32) if want_d2 else None
         som_map(self.h, X, n, b1, b2, d2)
         return b1, b2, d2
+
+    def train_batch(self, X, epochs: int, sigma0: float | None = None, kind: int = SOM_DECAY_GAUSSIAN,
+                    k: float = math.log(100.0), sigma_min: float = 1.0, cutoff: float = 1e-4, want_bmu: bool = True):
+        if sigma0 is None:
+            sigma0 = max(self.rows, self.cols) / 2.0
+        b = np.empty(X.shape[0], np.int32) if want_bmu else None
+        som_train_batch(self.h, X, X.shape[0], epochs, sigma0, som_schedule(kind, k, sigma_min, cutoff), b)
+        return b
+
+    def train_batch_csr(self, rowptr, col, val, n: int, epochs: int, sigma0: float | None = None,
+                        kind: int = SOM_DECAY_GAUSSIAN, k: float = math.log(100.0), sigma_min: float = 1.0,
+                        cutoff: float = 1e-4, want_bmu: bool = True):
+        if sigma0 is None:
+            sigma0 = max(self.rows, self.cols) / 2.0
+        b = np.empty(n, np.int32) if want_bmu else None
+        som_train_batch_csr(self.h, rowptr, col, val, n, epochs, sigma0, som_schedule(kind, k, sigma_min, cutoff), b)
+        return b
 
     def map_csr(self, rowptr, col, val, n: int, want_bmu2: bool = True, want_d2: bool = True):
         b1 = np.empty(n, np.int32)
