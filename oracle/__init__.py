@@ -65,6 +65,8 @@ def lib():
         L.or_map_csr.argtypes = [P, P, i64, i64, P, P, P, i64, P, P, P, P, P]
         L.or_train_batch.restype = ctypes.c_int
         L.or_train_batch.argtypes = [P, i32, i32, i32, i64, P, i64, i32, f64, i32, f64, f64, f64, P]
+        L.or_tfidf_csr.restype = None
+        L.or_tfidf_csr.argtypes = [P, P, P, i64, i64, P, P]
         L.or_row_sqnorm.restype = None
         L.or_row_sqnorm.argtypes = [P, i64, i64, P]
         L.or_qerror_from_d1.restype = f64
@@ -163,6 +165,17 @@ def train_batch(W, rows, cols, topo, X, epochs, sigma0, kind=DECAY_GAUSSIAN, k=L
     return W, b
 
 
+def tfidf_csr(rowptr, col, counts, d):
+    """Eq. 2 TF-IDF + L2 row normalisation (R28).  Returns (values, zero_rows)."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    counts = _f32(counts)
+    out = np.empty_like(counts)
+    zr = ctypes.c_int64()
+    lib().or_tfidf_csr(_p(rowptr), _p(col), _p(counts), rowptr.shape[0] - 1, d, _p(out), ctypes.byref(zr))
+    return out, zr.value
+
+
 def map_docs(W, X, want_margins=False):
     W, X = _f32(W), _f32(X)
     N, d = W.shape
@@ -197,6 +210,9 @@ def map_docs_csr(W, rowptr, col, val, want_margins=False):
     if want_margins:
         return b1, b2, d1, m12, m23
     return b1, b2, d1
+
+
+from .upstream import linear_init, map_geometry, pca_top2  # noqa: E402,F401
 
 
 def qerror_from_d1(d1) -> float:

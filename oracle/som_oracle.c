@@ -395,6 +395,44 @@ void or_umatrix(const float *W, int32_t rows, int32_t cols, int32_t topo,
     }
 }
 
+/* ------------------------------------------------------------ TF-IDF */
+/* Eq. 2 and the row normalisation of P:174, reading R28:
+ *   df_t   = #{documents d : tf(d,t) > 0},
+ *   idf_t  = ln(n / df_t)                      (natural log),
+ *   w_dt   = tf(d,t) idf_t / ||(tf(d,.) idf)||_2,
+ * products and the norm in fp64 (sum over the row's entries in order),
+ * one rounding to fp32.  The CSR pattern is kept (an entry whose idf is 0
+ * stays as an explicit 0); a row whose norm is 0 stays all-zero and is
+ * counted in *zero_rows.  counts: raw term frequencies. */
+void or_tfidf_csr(const int64_t *rowptr, const int32_t *col, const float *counts,
+                  int64_t n, int64_t d, float *out, int64_t *zero_rows)
+{
+    int64_t *df = (int64_t *)calloc((size_t)d, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p)
+            if (counts[p] > 0.0f) df[col[p]] += 1;
+    int64_t zr = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double ss = 0.0;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+            int64_t t = col[p];
+            double idf = df[t] > 0 ? log((double)n / (double)df[t]) : 0.0;
+            double v = (double)counts[p] * idf;
+            ss += v * v;
+        }
+        double nrm = sqrt(ss);
+        if (nrm == 0.0) ++zr;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+            int64_t t = col[p];
+            double idf = df[t] > 0 ? log((double)n / (double)df[t]) : 0.0;
+            double v = (double)counts[p] * idf;
+            out[p] = (nrm > 0.0) ? (float)(v / nrm) : 0.0f;
+        }
+    }
+    if (zero_rows) *zero_rows = zr;
+    free(df);
+}
+
 /* threads the OpenMP regions above will use (for cpu_baseline reporting) */
 int or_num_threads(void)
 {

@@ -383,3 +383,80 @@ def test_batch_fixed_point_and_zero_epochs():
     np.testing.assert_allclose(W, np.repeat(x, 9, axis=0), rtol=0, atol=1e-7)
     W3, _ = oracle.train_batch(W0, 3, 3, 0, X, 0, 1.5)
     assert np.array_equal(W3, W0)
+
+
+# ------------------------------------------------- upstream (NEXT-3: R28-R31)
+def _csr(rows, d):
+    indptr = [0]
+    col, val = [], []
+    for r in rows:
+        for t, c in sorted(r.items()):
+            col.append(t)
+            val.append(c)
+        indptr.append(len(col))
+    return (np.array(indptr, np.int64), np.array(col, np.int32), np.array(val, np.float32))
+
+
+def test_tfidf_spec_examples():
+    """IDF = ln(N/df) (ln 10 = 2.302585 for df = 1 of 10); a term in
+    every document weighs 0; L2 normalisation [3,4] -> [0.6, 0.8], [5] -> [1]."""
+    # doc0: a x3, b x4; doc1: c x1 -> idf(a) = idf(b) = idf(c) = ln 2
+    rp, ci, va = _csr([{0: 3, 1: 4}, {2: 1}], 3)
+    out, zr = oracle.tfidf_csr(rp, ci, va, 3)
+    assert out.tolist() == [_f32(0.6), _f32(0.8), 1.0] and zr == 0
+    # z (term 2) in every document: explicit zero; doc2 has only z: a zero row
+    rp, ci, va = _csr([{0: 1, 2: 5}, {1: 2, 2: 1}, {2: 7}], 3)
+    out, zr = oracle.tfidf_csr(rp, ci, va, 3)
+    assert out.tolist() == [1.0, 0.0, 1.0, 0.0, 0.0] and zr == 1
+    # ln 10: term 0 in one document of ten, together with term 1 (in all ten):
+    rows = [{0: 2, 1: 1}] + [{1: 1, 2 + i: 1} for i in range(9)]
+    rp, ci, va = _csr(rows, 11)
+    out, _ = oracle.tfidf_csr(rp, ci, va, 11)
+    assert out[0] == 1.0 and out[1] == 0.0          # 2 ln 10 / |2 ln 10|, and idf 0
+    # two terms with different idf: doc0 = (a:1, b:1), a in 2 of 4 docs (ln 2), b in 1 (ln 4 = 2 ln 2)
+    rp, ci, va = _csr([{0: 1, 1: 1}, {0: 1}, {2: 1}, {3: 1}], 4)
+    out, _ = oracle.tfidf_csr(rp, ci, va, 4)
+    assert out[0] == _f32(1 / math.sqrt(5)) and out[1] == _f32(2 / math.sqrt(5))
+
+
+def test_pca_spec_examples_and_invariants():
+    pc1, pc2, v1, v2, mu = oracle.pca_top2(np.array([[1, 0], [-1, 0], [2, 0], [-2, 0]], np.float64))
+    assert np.allclose(v1, [1, 0]) and abs(pc2) < 1e-12 and abs(pc1 - 10.0 / 3.0) < 1e-12   # var = 10/3
+    pc1, pc2, v1, v2, mu = oracle.pca_top2(np.array([[1, 0], [0, 1], [-1, 0], [0, -1]], np.float64))
+    assert abs(pc1 - pc2) < 1e-12 and abs(pc1 - 2.0 / 3.0) < 1e-12
+    X = uniform_matrix(50, 8, 3).astype(np.float64)
+    pc1, pc2, v1, v2, mu = oracle.pca_top2(X)
+    Xc = X - X.mean(0)
+    # the eigenvalue is the variance of the projection (closed form), maximal over directions
+    assert abs(np.var(Xc @ v1, ddof=1) - pc1) < 1e-12 and abs(np.var(Xc @ v2, ddof=1) - pc2) < 1e-12
+    assert abs(v1 @ v2) < 1e-12 and abs(np.linalg.norm(v1) - 1) < 1e-12
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        u = rng.normal(size=8)
+        u /= np.linalg.norm(u)
+        assert np.var(Xc @ u, ddof=1) <= pc1 + 1e-12
+        u -= (u @ v1) * v1
+        u /= np.linalg.norm(u)
+        assert np.var(Xc @ u, ddof=1) <= pc2 + 1e-12       # second largest on the complement of v1
+    assert v1[np.argmax(np.abs(v1))] > 0 and v2[np.argmax(np.abs(v2))] > 0          # R29 sign rule
+
+
+def test_linear_init_plane_and_corners():
+    X = uniform_matrix(80, 6, 5).astype(np.float64)
+    pc1, pc2, v1, v2, mu = oracle.pca_top2(X)
+    W = oracle.linear_init(4, 5, mu, v1, v2, pc1, pc2).astype(np.float64)
+    B = np.stack([v1, v2])
+    resid = (W - mu) - ((W - mu) @ B.T) @ B
+    assert np.abs(resid).max() < 1e-6                       # on the principal plane (fp32 rounding)
+    np.testing.assert_allclose(W[0], mu - math.sqrt(pc1) * v1 - math.sqrt(pc2) * v2, atol=1e-6)
+    np.testing.assert_allclose(W[19], mu + math.sqrt(pc1) * v1 + math.sqrt(pc2) * v2, atol=1e-6)
+    W1 = oracle.linear_init(1, 1, mu, v1, v2, pc1, pc2)
+    assert np.array_equal(W1[0], mu.astype(np.float32))   # 1x1 map: the mean
+
+
+def test_map_geometry_fig2_traces():
+    """S:152-160 hand traces of Fig. 2."""
+    assert oracle.map_geometry(400, 1.0, 1.0) == (9, 11, 20800)
+    assert oracle.map_geometry(4, 1.0, 1.0) == (3, 3, 1808)
+    r, c, _ = oracle.map_geometry(100, 10.0, 0.05)       # pc2 * munits < pc1 -> r = 1
+    assert (r, c) == oracle.map_geometry(100, 1.0, 1.0)[:2] == (6, 8)
