@@ -196,6 +196,43 @@ som_status som_comm_mailbox_ptr(som_ctx *h, void **mailbox);
  * NULL disables. */
 som_status som_set_trace(som_ctx *h, void *device_buf, int32_t steps);
 
+/* ---- Upstream steps: from a raw document-term matrix to an
+ * initialised map, on the device. */
+
+/* Eq. 2 TF-IDF + L2 row normalisation, reading R28:
+ * idf_t = ln(n / df_t), df_t = #rows with a positive count of t; out[p] =
+ * RN32(counts[p] idf_t / ||row||), products and norm in fp64; the CSR
+ * pattern is kept; rows whose norm is 0 stay 0 and are counted in
+ * *zero_rows (nullable).  Columns index [0, dim) of the handle's map.
+ * out: nnz floats, host or device. */
+som_status som_tfidf_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col, const float *counts,
+                         int64_t n, float *out, int64_t *zero_rows);
+
+/* Top-2 principal components of the rows (Fig. 2 step 3),
+ * reading R29: eigenpairs of the sample covariance (1/(n-1)) sum_i
+ * (x_i - mu)(x_i - mu)^T by subspace iteration on the implicitly centred
+ * covariance (never formed); each eigenvector signed so that its largest-
+ * magnitude component is positive.  Outputs (host or device, fp64): mean
+ * (dim), v1, v2 (dim), pc[2] = (pc1, pc2).  n >= 2. */
+som_status som_pca_top2(som_ctx *h, const float *X, int64_t n, double *mean, double *v1, double *v2,
+                        double *pc);
+som_status som_pca_top2_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col, const float *val,
+                            int64_t n, double *mean, double *v1, double *v2, double *pc);
+
+/* PCA-plane linear initialisation ("a regular, two-dimensional
+ * sequence of vectors taken along a hyperplane spanned by the two largest
+ * principal components"), reading R30: unit (i, j) = mean + a_j sqrt(pc1) v1
+ * + b_i sqrt(pc2) v2, a_j = -1 + 2j/(cols-1), b_i = -1 + 2i/(rows-1) (0 for
+ * one column / row), fp64, RN32.  Inputs fp64, host or device. */
+som_status som_init_linear(som_ctx *h, const double *mean, const double *v1, const double *v2, double pc1,
+                           double pc2);
+
+/* Fig. 2, reading R31: map rows <= cols and the iteration count
+ * numItr = ceil(50 nn/m) m 4 for m records with top eigenvalues pc1 >= pc2.
+ * Pure host arithmetic; m >= 1. */
+som_status som_map_geometry(int64_t m, double pc1, double pc2, int32_t *rows, int32_t *cols,
+                            int64_t *num_itr);
+
 /* Batch SOM (R27: Kohonen's batch map; the variant of the
  * GPU SOMs the paper reviews).  Per epoch e in [0, epochs),
  * with the current W: c_i = BMU of every row (exact mapping, R10 / R25),

@@ -38,8 +38,8 @@ def pca_top2(X):
     C = (Xc.T @ Xc) / (n - 1)
     w, V = np.linalg.eigh(C)               # ascending eigenvalues
     pc1, pc2 = float(w[-1]), float(max(w[-2], 0.0)) if X.shape[1] > 1 else 0.0
-    v1 = _sign_fix(V[:, -1])
-    v2 = _sign_fix(V[:, -2]) if X.shape[1] > 1 else np.zeros_like(v1)
+    v1 = np.ascontiguousarray(_sign_fix(V[:, -1]))
+    v2 = np.ascontiguousarray(_sign_fix(V[:, -2])) if X.shape[1] > 1 else np.zeros_like(v1)
     return pc1, pc2, v1, v2, mu
 
 
@@ -57,9 +57,9 @@ def linear_init(rows, cols, mu, v1, v2, pc1, pc2):
 
 def map_geometry(m, pc1, pc2):
     """Fig. 2: (nrows, ncols, numItr) for m records with eigenvalues pc1 >= pc2."""
-    munits = int(round(5.0 * math.sqrt(m)))                                  # step 2
+    munits = int(math.floor(5.0 * math.sqrt(m) + 0.5))                       # step 2 (nearest, halves up)
     r = 1.0 if (pc1 == 0.0 or pc2 * munits < pc1) else math.sqrt(pc1 / pc2)  # steps 5-8
-    size1 = max(1, int(round(min(munits, math.sqrt(munits / (r * math.sqrt(0.75)))))))   # step 9
+    size1 = max(1, int(math.floor(min(munits, math.sqrt(munits / (r * math.sqrt(0.75)))) + 0.5)))   # step 9
     size2 = munits // size1                                                  # step 10
     nrows, ncols = min(size1, size2), max(size1, size2)                      # steps 11-12
     nn = nrows * ncols                                                       # step 13

@@ -228,6 +228,38 @@ cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* co
 cudaError_t launch_batch_update(const double* S, double* num, int N, int d, int rows, int cols, int topo,
                                 double sigma, double r2, float* W, cudaStream_t st);
 
+// Upstream steps (upstream.cu, R28-R30): TF-IDF + L2 rows; top-2 PCA by
+// subspace iteration (block kPcaBlock) on the implicitly centred covariance;
+// PCA-plane linear init.
+constexpr int kPcaBlock = 8;
+cudaError_t launch_tfidf(const int64_t* rowptr, const int32_t* col, const float* cnt, int64_t n, int d, int64_t nnz,
+                         int* df, double* idf, float* out, unsigned long long* zero_rows, cudaStream_t st);
+struct PcaInput {
+    const float* X;          // dense n x d rows, or null for CSR
+    const int64_t* rowptr;   // CSR (rowptr[0] == 0)
+    const int32_t* col;
+    const float* val;
+    int64_t n;
+    int d;
+    const int* cptr;         // column-major copy: d + 1 offsets
+    const int32_t* cent;     // entries in column order (rows ascending within a column)
+    const int32_t* erow;     // row of each entry
+};
+size_t pca_csc_temp_bytes(int64_t nnz, int d);
+cudaError_t launch_pca_csc(const int64_t* rowptr, const int32_t* col, int64_t n, int d, int64_t nnz, int* cptr,
+                           int32_t* cent, int32_t* erow, int32_t* scratch, void* temp, size_t temp_bytes,
+                           cudaStream_t st);
+cudaError_t launch_pca_mean(const PcaInput& x, double* mu, cudaStream_t st);
+cudaError_t launch_pca_init_q(double* Q, int d, uint64_t seed, cudaStream_t st);
+cudaError_t launch_pca_apply(const PcaInput& x, const double* mu, double* Q, double* Y, double* Z, int orth,
+                             cudaStream_t st);
+cudaError_t launch_pca_orth(double* Z, double* Q, int d, cudaStream_t st);
+cudaError_t launch_pca_rr(const PcaInput& x, const double* mu, double* Q, double* Y, double* Z, double* out,
+                          cudaStream_t st);
+cudaError_t launch_pca_extract(const double* Q, int d, double* v1, double* v2, cudaStream_t st);
+cudaError_t launch_init_linear(float* W, int rows, int cols, int d, const double* mu, const double* v1,
+                               const double* v2, double pc1, double pc2, cudaStream_t st);
+
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);

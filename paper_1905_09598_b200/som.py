@@ -43,7 +43,8 @@ _lib = None
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
            "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_map", "som_map_csr", "som_set_map_precision",
-           "som_train_batch", "som_train_batch_csr",
+           "som_train_batch", "som_train_batch_csr", "som_tfidf_csr", "som_pca_top2", "som_pca_top2_csr",
+           "som_init_linear", "som_map_geometry",
            "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
            "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
@@ -67,6 +68,11 @@ def lib():
         "som_train_online": [P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
         "som_train_online_csr": [P, P, P, P, i64, i32, f64, f64, P, u64, i64, i64, P],
         "som_train_batch": [P, P, i64, i32, f64, P, P],
+        "som_tfidf_csr": [P, P, P, P, i64, P, P],
+        "som_pca_top2": [P, P, i64, P, P, P, P],
+        "som_pca_top2_csr": [P, P, P, P, i64, P, P, P, P],
+        "som_init_linear": [P, P, P, P, f64, f64],
+        "som_map_geometry": [i64, f64, f64, P, P, P],
         "som_train_batch_csr": [P, P, P, P, i64, i32, f64, P, P],
         "som_map": [P, P, i64, P, P, P],
         "som_map_csr": [P, P, P, P, i64, P, P, P],
@@ -124,7 +130,8 @@ def _ptr(a, dtype=None, writable=False):
         if not a.is_contiguous():
             raise ValueError("tensor must be contiguous")
         if dtype is not None:
-            want = {np.float32: "torch.float32", np.int32: "torch.int32", np.int64: "torch.int64"}[dtype]
+            want = {np.float32: "torch.float32", np.int32: "torch.int32", np.int64: "torch.int64",
+                    np.float64: "torch.float64"}[dtype]
             if str(a.dtype) != want:
                 raise TypeError(f"expected {want}, got {a.dtype}")
         return a.data_ptr()
@@ -186,6 +193,34 @@ def som_train_batch_csr(h, rowptr, col, val, n: int, epochs: int, sigma0: float,
     _check(lib().som_train_batch_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                                      epochs, sigma0, ctypes.byref(sched) if sched is not None else None,
                                      _ptr(bmu, np.int32, True)))
+
+
+def som_tfidf_csr(h, rowptr, col, counts, n: int, out) -> int:
+    z = ctypes.c_int64()
+    _check(lib().som_tfidf_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(counts, np.float32), n,
+                               _ptr(out, np.float32, True), ctypes.byref(z)))
+    return z.value
+
+
+def som_pca_top2(h, X, n: int, mean, v1, v2, pc) -> None:
+    _check(lib().som_pca_top2(h, _ptr(X, np.float32), n, _ptr(mean, np.float64, True), _ptr(v1, np.float64, True),
+                              _ptr(v2, np.float64, True), _ptr(pc, np.float64, True)))
+
+
+def som_pca_top2_csr(h, rowptr, col, val, n: int, mean, v1, v2, pc) -> None:
+    _check(lib().som_pca_top2_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                                  _ptr(mean, np.float64, True), _ptr(v1, np.float64, True),
+                                  _ptr(v2, np.float64, True), _ptr(pc, np.float64, True)))
+
+
+def som_init_linear(h, mean, v1, v2, pc1: float, pc2: float) -> None:
+    _check(lib().som_init_linear(h, _ptr(mean, np.float64), _ptr(v1, np.float64), _ptr(v2, np.float64), pc1, pc2))
+
+
+def som_map_geometry(m: int, pc1: float, pc2: float) -> tuple[int, int, int]:
+    r, c, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    _check(lib().som_map_geometry(m, pc1, pc2, ctypes.byref(r), ctypes.byref(c), ctypes.byref(t)))
+    return r.value, c.value, t.value
 
 
 def som_map(h, X, n: int, bmu1, bmu2=None, d2=None) -> None:
@@ -383,6 +418,18 @@ class SOM:
         b = np.empty(n, np.int32) if want_bmu else None
         som_train_batch_csr(self.h, rowptr, col, val, n, epochs, sigma0, som_schedule(kind, k, sigma_min, cutoff), b)
         return b
+
+    def pca_top2(self, X=None, csr=None):
+        """(pc1, pc2, v1, v2, mean) of dense rows X or csr = (rowptr, col, val, n)."""
+        mean, v1, v2, pc = np.empty(self.dim), np.empty(self.dim), np.empty(self.dim), np.empty(2)
+        if csr is not None:
+            som_pca_top2_csr(self.h, *csr[:3], csr[3], mean, v1, v2, pc)
+        else:
+            som_pca_top2(self.h, X, X.shape[0], mean, v1, v2, pc)
+        return float(pc[0]), float(pc[1]), v1, v2, mean
+
+    def init_linear(self, mean, v1, v2, pc1: float, pc2: float):
+        som_init_linear(self.h, mean, v1, v2, pc1, pc2)
 
     def map_csr(self, rowptr, col, val, n: int, want_bmu2: bool = True, want_d2: bool = True):
         b1 = np.empty(n, np.int32)
