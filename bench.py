@@ -153,7 +153,7 @@ def conv_peak_per_s():
     return 16 * 148 * 1965e6, "nominal 16 F2F/clk/SM x 148 x 1965 MHz (no measurement file)"
 
 
-def mapping_leg(som, torch, args, local, seed):
+def mapping_leg(som, torch, args, local, seed, world=1, rank=0):
     """Batch BMU mapping docs/s on a c5-shaped sample (BASELINE.json configs[4]:
     100x100 map, 20k terms, CSR documents; the full 10M-document job is the
     doc-sharded multi-GPU case) through som_map_csr.  Main: the default (AUTO)
@@ -163,7 +163,7 @@ def mapping_leg(som, torch, args, local, seed):
     cfg = CONFIGS["c5"]
     n, d, N = args.map_docs, cfg["d"], cfg["rows"] * cfg["cols"]
     C = bank_corpus(n, d, seed=seed + 500)
-    Wsrc = bank_corpus(N, d, seed=seed + 501).dense()
+    Wsrc = bank_corpus(N, d, seed=args.seed + 501).dense()     # the map is replicated on every rank
     W = (0.5 * Wsrc + 0.5 / np.sqrt(d)).astype(np.float32)
     del Wsrc
     mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
@@ -188,6 +188,18 @@ def mapping_leg(som, torch, args, local, seed):
 
     ms, launches = timed(som.SOM_MAP_AUTO)
     sp_b1 = b1.cpu().numpy()
+    # document sharding: every rank maps its own n documents;
+    # the job time is the slowest rank's, the error sums are all-reduced
+    qe_l, te_l = som.som_errors_csr(mm.h, rp, ci, va, n)
+    err_ms, _, _ = som.som_last_stats(mm.h)
+    ms_max, qe, te = ms, qe_l, te_l
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1905_09598_b200 import dist as sdist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        qe, te = sdist.reduce_errors(qe_l, te_l, n, device=torch.device("cuda", local))
     ms_tc, launches_tc = timed(som.SOM_MAP_3XTF32)
     agree = float(np.mean(b1.cpu().numpy() == sp_b1))
     mm.close()
@@ -198,7 +210,7 @@ def mapping_leg(som, torch, args, local, seed):
     executed = 3.0 * flop / (ms_tc / 1000.0) / 1e12
 
     cpu = None
-    if not args.no_baseline:
+    if not args.no_baseline and rank == 0:
         import oracle
         ns = min(n, 10000)
         t0 = time.perf_counter()
@@ -207,10 +219,12 @@ def mapping_leg(som, torch, args, local, seed):
         cpu = {"value": ns / dt, "unit": "docs/s", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": f"first {ns} documents, fp64 sparse-identity oracle (or_map_csr, OpenMP over docs), "
                          f"{dt:.1f} s"}
-    return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms",
-            "docs_per_s": n / (ms / 1000.0), "ms": ms, "launches": launches,
+    return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms "
+                        f"per GPU, document-sharded over {world} GPU(s)",
+            "docs_per_s": world * n / (ms_max / 1000.0), "ms": ms_max, "launches": launches, "n_gpus": world,
+            "scaling": "weak", "qe": qe, "te": te, "errors_ms_rank0": err_ms,
             "path": "exact fp64 sparse identity (SOM_MAP_SPARSE_F64, AUTO)",
-            "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T>",
+            "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T> (rank 0)",
                          "achieved": fma / (ms / 1000.0) / 1e12, "peak": cpk / 1e12, "unit": "T conv+FMA/s",
                          "frac": fma / (ms / 1000.0) / cpk, "peak_source": cpk_src,
                          "work": "nnz*N fp32->fp64 conversions + fp64 FMAs per call (one per non-zero per unit), "
@@ -493,7 +507,7 @@ def run_b200(args, rank, world, local):
     g_used, k_used = som.som_last_train_config(m.h)
     kname = {0: "som_train_kernel (W global)", 1: "som_train_kernel (W smem)",
              2: "som_train_reg_kernel (W registers)"}.get(k_used, "?")
-    mapping = mapping_leg(som, torch, args, local, seed) if args.map_docs > 0 else None
+    mapping = mapping_leg(som, torch, args, local, seed, world, rank) if args.map_docs > 0 else None
     train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
     table3 = table3_leg(som, torch, args, local, seed) if args.table3_steps > 0 else None
     batch = batch_leg(som, torch, args, local, seed) if args.batch_epochs > 0 else None

@@ -616,10 +616,14 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     if (smem > (size_t)h->max_smem_optin)
         return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
 
-    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.G + 64, h->stream));
+    // exchange slots: two parities of G slots, each parity on its own 256-byte
+    // lines (a line shared by step t's and step t+1's slots would be written
+    // by fast CTAs while slow ones still poll it)
+    a.xstride = (a.G + 31) & ~31;
+    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
     a.xchg = (unsigned long long*)h->xchg.p;
-    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.G);
-    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.G + 64, h->stream));
+    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.xstride);
+    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
 
     const int64_t steps = t_end - t_begin;
     bool log_dev = bmu_log && is_device_ptr(bmu_log);

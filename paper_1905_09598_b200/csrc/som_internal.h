@@ -24,6 +24,7 @@ struct TrainArgs {
     int rows, cols, topo;
     int N;                     // rows * cols
     int G;                     // grid size (co-resident CTAs)
+    int xstride;               // slots per exchange parity: G rounded up to 32 (parities on separate lines)
     int S;                     // max units per CTA = ceil(N / G)
     int64_t t0, t1;            // step range
     uint64_t seed;
@@ -80,7 +81,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned 
 __device__ __forceinline__ unsigned long long xchg_tag(int64_t t) { return 0x80ull | (unsigned long long)(t & 0x7F); }
 
 __device__ __forceinline__ void xchg_publish(const TrainArgs& a, unsigned long long key, int64_t t, int b, int lane) {
-    if (lane == 0) st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.G + b, (key & ~0xFFull) | xchg_tag(t));
+    if (lane == 0) st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.xstride + b, (key & ~0xFFull) | xchg_tag(t));
 }
 
 __device__ __forceinline__ bool xchg_should_stop(const TrainArgs& a, unsigned& spins, int lane) {
@@ -95,7 +96,7 @@ __device__ __forceinline__ bool xchg_should_stop(const TrainArgs& a, unsigned& s
 
 __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int64_t t, int b, int lane, int* stop) {
     const unsigned long long tag = xchg_tag(t);
-    const unsigned long long* slots = a.xchg + (size_t)(t & 1) * a.G;
+    const unsigned long long* slots = a.xchg + (size_t)(t & 1) * a.xstride;
     unsigned long long gmin = 0;
     unsigned spins = 0;
     for (;;) {
