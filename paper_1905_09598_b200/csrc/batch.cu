@@ -5,8 +5,9 @@
 //   1. BMUs of all documents (the exact mapping paths, R10 / R25);
 //   2. documents bucketed by BMU with a stable radix sort of (c_i, i), so
 //      every bucket lists its documents in index order;
-//   3. S_c = sum_{i: c_i = c} x_i and n_c in fp64, one CTA per unit adding
-//      its documents in index order (deterministic, no atomics);
+//   3. S_c = sum_{i: c_i = c} x_i and n_c in fp64, in document order
+//      (dense rows: one CTA per unit; CSR: entries grouped by (unit, column)
+//      with a stable sort, one thread per group) — deterministic, no atomics;
 //   4. num_u = sum_c h(u, c) [S_c | n_c] — an N x N x (d+1) contraction with
 //      the lattice kernel generated on the fly from separable tables (R26);
 //      tiles whose row span is outside the cutoff radius are skipped;
@@ -49,28 +50,72 @@ __global__ void accumulate_dense_kernel(const float* __restrict__ X, int d, cons
     if (threadIdx.x == 0) row[d] = (double)m;
 }
 
-// the same from CSR rows: the row of S is zeroed, then each document's
-// non-zeros (distinct columns) are added, documents in index order
-__global__ void accumulate_csr_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                      const float* __restrict__ val, int d, const int32_t* __restrict__ order,
-                                      const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, int dp,
-                                      double* __restrict__ S) {
-    const int c = blockIdx.x;
-    double* row = S + (size_t)c * dp;
-    const int o = off[c], m = cnt[c];
-    for (int k = threadIdx.x; k < d; k += blockDim.x) row[k] = 0.0;
-    __syncthreads();
-    for (int q = 0; q < m; ++q) {
-        const int64_t i = order[o + q];
-        for (int64_t p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) row[col[p]] += (double)val[p];
-        __syncthreads();
+// CSR rows: every non-zero gets the key (c_i * d + col); a stable radix
+// sort of the keys over the entries (which are in document order) groups
+// the entries of one (unit, column) pair, documents ascending, and one
+// thread per group adds them in that order (balanced even when one unit
+// collects thousands of documents; deterministic).
+__global__ void entry_keys_kernel(const int64_t* rowptr, const int32_t* col, int64_t n, const int32_t* bmu, int d,
+                                  uint32_t* key, int32_t* idx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t base = (uint32_t)bmu[i] * (uint32_t)d;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+            key[p] = base + (uint32_t)col[p];
+            idx[p] = (int32_t)p;
+        }
     }
-    if (threadIdx.x == 0) row[d] = (double)m;
 }
 
-// num[u][k] = sum_c h(u, c) S[c][k]; 64 units x 64 columns per CTA, 16 units
-// c per step, 4 x 4 outputs per thread; h from the separable tables (R26).
-constexpr int GM = 64, GN = 64, GK = 16, GT = 256;
+// groups of <= 32 entries: one thread adds them in order; longer groups (a
+// frequent term in a crowded unit) go to a list for the warp kernel below
+constexpr int kShortGroup = 32;
+__global__ void segment_sum_kernel(const uint32_t* key, const int32_t* idx, const float* val, int64_t nnz, int d,
+                                   int dp, double* S, int32_t* longs, int* nlong) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key[e];
+        if (e > 0 && key[e - 1] == k) continue;          // not the first entry of its group
+        int64_t f = e + 1;
+        while (f < nnz && f - e <= kShortGroup && key[f] == k) ++f;
+        if (f - e > kShortGroup) {                       // long group: handled by a warp
+            longs[atomicAdd(nlong, 1)] = (int32_t)e;
+            continue;
+        }
+        double s = 0.0;
+        for (int64_t g = e; g < f; ++g) s += (double)val[idx[g]];
+        S[(size_t)(k / (uint32_t)d) * dp + (k % (uint32_t)d)] = s;
+    }
+}
+
+// one warp per long group: lane j adds entries j, j+32, ... in order, then a
+// fixed xor butterfly (the list order varies run to run, each sum does not)
+__global__ void long_segment_kernel(const uint32_t* key, const int32_t* idx, const float* val, int64_t nnz, int d,
+                                    int dp, double* S, const int32_t* longs, const int* nlong) {
+    const int lane = threadIdx.x & 31;
+    const int nl = *nlong;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nl; w += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t e = longs[w];
+        const uint32_t k = key[e];
+        double s = 0.0;
+        bool more = true;
+        for (int64_t f = e + lane; __any_sync(0xffffffffu, more); f += 32) {
+            more = f < nnz && key[f] == k;
+            if (more) s += (double)val[idx[f]];
+        }
+        s = warp_sum_f64(s);
+        if (lane == 0) S[(size_t)(k / (uint32_t)d) * dp + (k % (uint32_t)d)] = s;
+    }
+}
+
+__global__ void counts_col_kernel(const int32_t* cnt, int N, int d, int dp, double* S) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
+        S[(size_t)c * dp + d] = (double)cnt[c];
+}
+
+// num[u][k] = sum_c h(u, c) S[c][k]; 128 units x 64 columns per CTA, 16
+// units c per step, 8 x 4 outputs per thread (12 shared-memory wavefronts per
+// 1024 DFMAs, so the FP64 pipe, not shared memory, bounds the loop); h from
+// the separable tables (R26).
+constexpr int GM = 128, GN = 64, GK = 16, GT = 256, TI = GM / 16, TJ = GN / 16;
 
 struct GemmArgs {
     const double* S;   // N x dp
@@ -99,11 +144,18 @@ __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
 
     const int u0 = blockIdx.y * GM, k0 = blockIdx.x * GN;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4];
+    // lattice coordinates of the tile's units (fixed) and of each K step's units
+    __shared__ int ui[GM], uj[GM], ci[GK], cj[GK];
+    for (int t = threadIdx.x; t < GM; t += GT) {
+        const int u = min(u0 + t, a.N - 1);
+        ui[t] = u / a.cols;
+        uj[t] = u - ui[t] * a.cols;
+    }
+    double acc[TI][TJ];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < TJ; ++j) acc[i][j] = 0.0;
     // lattice rows spanned by this unit tile (for the cutoff skip)
     const int ulast = min(a.N, u0 + GM) - 1;
     const int ur0 = u0 / a.cols, ur1 = ulast / a.cols;
@@ -115,12 +167,18 @@ __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
         const double g2min = a.topo == 0 ? (double)gap * gap : 0.75 * ((double)gap * gap);
         if (g2min > a.r2) continue;   // block-uniform: no pair of the tiles is inside the cutoff
         __syncthreads();
+        if (threadIdx.x < GK) {
+            const int c = min(c0 + (int)threadIdx.x, a.N - 1);
+            ci[threadIdx.x] = c / a.cols;
+            cj[threadIdx.x] = c - ci[threadIdx.x] * a.cols;
+        }
+        __syncthreads();
         for (int e = threadIdx.x; e < GK * GM; e += GT) {
             const int cc = e / GM, uu = e - cc * GM;
             const int u = u0 + uu, c = c0 + cc;
             double h = 0.0;
             if (u < a.N && c < a.N) {
-                const int iu = u / a.cols, ju = u - iu * a.cols, ic = c / a.cols, jc = c - ic * a.cols;
+                const int iu = ui[uu], ju = uj[uu], ic = ci[cc], jc = cj[cc];
                 const int di = abs(iu - ic);
                 int dx;
                 double g2;
@@ -143,23 +201,23 @@ __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
         __syncthreads();
 #pragma unroll
         for (int cc = 0; cc < GK; ++cc) {
-            double hv[4], sv[4];
+            double hv[TI], sv[TJ];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) hv[i] = hs[cc][ty + 16 * i];
+            for (int i = 0; i < TI; ++i) hv[i] = hs[cc][ty + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) sv[j] = ss[cc][tx + 16 * j];
+            for (int j = 0; j < TJ; ++j) sv[j] = ss[cc][tx + 16 * j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < TI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(hv[i], sv[j], acc[i][j]);
+                for (int j = 0; j < TJ; ++j) acc[i][j] = fma(hv[i], sv[j], acc[i][j]);
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < TI; ++i) {
         const int u = u0 + ty + 16 * i;
         if (u >= a.N) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < TJ; ++j) {
             const int k = k0 + tx + 16 * j;
             if (k < a.dp) a.num[(size_t)u * a.dp + k] = acc[i][j];
         }
@@ -217,10 +275,41 @@ cudaError_t launch_batch_accumulate_dense(const float* X, int d, const int32_t* 
     return cudaGetLastError();
 }
 
-cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* col, const float* val, int d,
-                                        const int32_t* order, const int32_t* off, const int32_t* cnt, int N,
-                                        double* S, cudaStream_t st) {
-    accumulate_csr_kernel<<<N, 256, 0, st>>>(rowptr, col, val, d, order, off, cnt, d + 1, S);
+size_t batch_csr_temp_bytes(int64_t nnz) {
+    size_t a = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)nnz, 0, 32);
+    return a + 256;
+}
+
+// S_c for CSR rows by (unit, column) groups; work: 2 nnz u32 keys + 2 nnz int32 (inside `work`)
+cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                                        int64_t nnz, int d, const int32_t* bmu, const int32_t* cnt, int N, double* S,
+                                        void* work, void* temp, size_t temp_bytes, cudaStream_t st) {
+    uint32_t* key_in = (uint32_t*)work;
+    uint32_t* key_out = key_in + nnz;
+    int32_t* idx_in = (int32_t*)(key_out + nnz);
+    int32_t* idx_out = idx_in + nnz;
+    const int dp = d + 1;
+    cudaError_t e = cudaMemsetAsync(S, 0, sizeof(double) * (size_t)N * dp, st);
+    if (e != cudaSuccess) return e;
+    if (nnz > 0) {
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+        entry_keys_kernel<<<blocks, 256, 0, st>>>(rowptr, col, n, bmu, d, key_in, idx_in);
+        int bits = 1;
+        while (bits < 32 && ((uint64_t)1 << bits) < (uint64_t)N * (uint64_t)d) ++bits;
+        size_t tb = temp_bytes;
+        e = cub::DeviceRadixSort::SortPairs(temp, tb, key_in, key_out, idx_in, idx_out, (int)nnz, 0, bits, st);
+        if (e != cudaSuccess) return e;
+        int32_t* longs = (int32_t*)key_in;                 // key_in is free after the sort
+        int* nlong = (int*)(idx_in);                       // idx_in likewise (first word)
+        e = cudaMemsetAsync(nlong, 0, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        segment_sum_kernel<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(
+            key_out, idx_out, val, nnz, d, dp, S, longs, nlong);
+        long_segment_kernel<<<148 * 4, 256, 0, st>>>(key_out, idx_out, val, nnz, d, dp, S, longs, nlong);
+    }
+    counts_col_kernel<<<(N + 255) / 256, 256, 0, st>>>(cnt, N, d, dp, S);
     return cudaGetLastError();
 }
 

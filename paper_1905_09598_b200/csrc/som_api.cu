@@ -620,6 +620,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // lines (a line shared by step t's and step t+1's slots would be written
     // by fast CTAs while slow ones still poll it)
     a.xstride = (a.G + 31) & ~31;
+    a.poll_ns = 0;
+    if (const char* e = std::getenv("SOM_POLL_NS")) a.poll_ns = std::max(0, std::atoi(e));
     CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
     a.xchg = (unsigned long long*)h->xchg.p;
     a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.xstride);
@@ -1116,6 +1118,16 @@ som_status train_batch_impl(som_ctx* h, const float* Xd, const CsrIn* csr, int64
     void* temp = (void*)(((uintptr_t)(off + N) + 255) & ~(uintptr_t)255);
     const size_t plane = sizeof(double) * (size_t)N * (d + 1);
     CK(h->bS.ensure(plane, h->stream));
+    // CSR: per-entry (unit, column) keys for the segmented per-unit sums
+    size_t csr_tb = 0;
+    void* csr_temp = nullptr;
+    if (csr) {
+        if ((uint64_t)N * (uint64_t)d > 0xFFFFFFFFull) return fail(SOM_EUNSUPPORTED, "batch SOM: N * dim >= 2^32");
+        if (csr->nnz > INT32_MAX) return fail(SOM_EUNSUPPORTED, "batch SOM: nnz >= 2^31");
+        csr_tb = batch_csr_temp_bytes(csr->nnz);
+        CK(h->up.ensure(16 * (size_t)csr->nnz + csr_tb + 512, h->stream));
+        csr_temp = (void*)(((uintptr_t)((char*)h->up.p + 16 * (size_t)csr->nnz) + 255) & ~(uintptr_t)255);
+    }
     CK(h->bnum.ensure(plane, h->stream));
     // exact BMUs: the dense definition (R10), or the sparse identity (R25) for TF-IDF-like CSR rows
     const int saved = h->map_precision;
@@ -1138,8 +1150,8 @@ som_status train_batch_impl(som_ctx* h, const float* Xd, const CsrIn* csr, int64
         const double r2 = sd.cutoff > 0.0 ? 2.0 * sigma * sigma * std::log(1.0 / sd.cutoff) : INFINITY;
         if ((st = map_all(&launches))) break;
         CK(launch_batch_bucket(b, n, N, order, cnt, off, scratch, temp, tb, h->stream));
-        if (csr) CK(launch_batch_accumulate_csr(csr->rowptr, csr->col, csr->val, d, order, off, cnt, N,
-                                                (double*)h->bS.p, h->stream));
+        if (csr) CK(launch_batch_accumulate_csr(csr->rowptr, csr->col, csr->val, n, csr->nnz, d, b, cnt, N,
+                                                (double*)h->bS.p, h->up.p, csr_temp, csr_tb, h->stream));
         else CK(launch_batch_accumulate_dense(Xd, d, order, off, cnt, N, (double*)h->bS.p, h->stream));
         CK(launch_batch_update((const double*)h->bS.p, (double*)h->bnum.p, N, d, h->rows, h->cols, h->topo, sigma,
                                r2, h->W, h->stream));

@@ -25,6 +25,7 @@ struct TrainArgs {
     int N;                     // rows * cols
     int G;                     // grid size (co-resident CTAs)
     int xstride;               // slots per exchange parity: G rounded up to 32 (parities on separate lines)
+    int poll_ns;               // back-off between exchange polls (0: spin)
     int S;                     // max units per CTA = ceil(N / G)
     int64_t t0, t1;            // step range
     uint64_t seed;
@@ -109,6 +110,7 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
         }
         if (__all_sync(0xffffffffu, ok)) { gmin = warp_min_u64(m); break; }
         if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
+        if (a.poll_ns) __nanosleep(a.poll_ns);
     }
     if (a.world <= 1) return gmin;
     const size_t par = (size_t)(t & 1) * a.world;
@@ -223,9 +225,10 @@ cudaError_t launch_batch_bucket(const int32_t* bmu, int64_t n, int N, int32_t* o
                                 int32_t* scratch, void* temp, size_t temp_bytes, cudaStream_t st);
 cudaError_t launch_batch_accumulate_dense(const float* X, int d, const int32_t* order, const int32_t* off,
                                           const int32_t* cnt, int N, double* S, cudaStream_t st);
-cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* col, const float* val, int d,
-                                        const int32_t* order, const int32_t* off, const int32_t* cnt, int N,
-                                        double* S, cudaStream_t st);
+size_t batch_csr_temp_bytes(int64_t nnz);
+cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                                        int64_t nnz, int d, const int32_t* bmu, const int32_t* cnt, int N, double* S,
+                                        void* work, void* temp, size_t temp_bytes, cudaStream_t st);
 cudaError_t launch_batch_update(const double* S, double* num, int N, int d, int rows, int cols, int topo,
                                 double sigma, double r2, float* W, cudaStream_t st);
 
