@@ -290,3 +290,30 @@ def test_c2_shape_global_kernels_ring_and_registers(som, monkeypatch, ring):
     W0 = init_rows(X, 400, 1004)
     W, log, Wo, logo = _train_both(som, 20, 20, 1, X, W0, 100, 0.1, 10.0, 4, mode=2, t_end=1500)
     _assert_train(W, log, Wo, logo)
+
+
+@pytest.mark.parametrize("csr", [False, True])
+def test_c4_shape_prefix(som, csr):
+    """c4 map and vocabulary (100x100 hex, 20k terms; W = 800 MB streams from
+    HBM): the first 40 steps, dense rows (TMA row-ring kernel) and CSR rows
+    (sparse-distance kernel), against the oracle.  2,000 documents keep the
+    oracle's dense copy small; the kernels only see the map and row shapes."""
+    C = bank_corpus(2000, 20000, seed=44)
+    X = C.dense()
+    W0 = init_rows(X, 10000, 1044) if X.shape[0] >= 10000 else \
+        (0.5 * init_rows(bank_corpus(10000, 20000, seed=45).dense(), 10000, 1) + 0.5 * X.mean(0)).astype(np.float32)
+    steps = 40
+    with som.SOM(100, 100, 20000, 1) as m:
+        m.set_weights(W0)
+        log = np.empty(steps, np.int32)
+        if csr:
+            m.train_online_csr(C.indptr, C.indices, C.data, C.n, 2, alpha0=0.1, sigma0=50.0, seed=4, t_end=steps,
+                               bmu_log=log)
+        else:
+            m.train_online(X, epochs=2, alpha0=0.1, sigma0=50.0, seed=4, t_end=steps, bmu_log=log)
+        ms, _, _ = som.som_last_stats(m.h)
+        g, k = som.som_last_train_config(m.h)
+        W = m.get_weights()
+    Wo, logo = oracle.train_online(W0, 100, 100, 1, X, 2, 0.1, 50.0, 4, t_end=steps)
+    _assert_train(W, log, Wo, logo)
+    print(f" [c4 prefix {'csr' if csr else 'dense'}: kernel {k}, G={g}, {1000 * ms / steps:.1f} us/step]", end="")
