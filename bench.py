@@ -55,6 +55,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BENCH_ONE_DEVICE") == "1":   # test hook: every rank on cuda:0 (multi-rank plumbing check)
+        local = 0
     return rank, world, local
 
 
@@ -403,7 +405,11 @@ def run_b200(args, rank, world, local):
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")   # gloo: plumbing check with ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     seed = args.seed + rank                     # independent problem per rank
     cfg, C = workload(args.config, seed, args.epochs)
     n, d, N = cfg["n"], cfg["d"], cfg["rows"] * cfg["cols"]
