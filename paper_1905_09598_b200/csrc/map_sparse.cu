@@ -46,15 +46,25 @@ __device__ __forceinline__ void top2_ins(unsigned long long& k1, unsigned long l
     else if (v < k2) { k2 = v; }
 }
 
-// W (N x d fp32, row-major) -> WT (d x Np, fp64 or fp32); columns u >= N are zero.
+// W (N x d fp32, row-major) -> WT (d x Np, fp64 or fp32); columns u >= N
+// are zero, -0 becomes +0 (same products), and *flag is set if any value is
+// negative, subnormal, infinite or NaN (then the integer widening below may
+// not be used).
 template <typename T>
-__global__ void wt_kernel(const float* __restrict__ W, int N, int d, int Np, T* __restrict__ WT) {
+__global__ void wt_kernel(const float* __restrict__ W, int N, int d, int Np, T* __restrict__ WT, int* flag) {
     __shared__ float tile[32][33];
     const int u0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    bool bad = false;
     for (int r = threadIdx.y; r < 32; r += 8) {
         const int u = u0 + r, k = k0 + threadIdx.x;
-        tile[r][threadIdx.x] = (u < N && k < d) ? W[(int64_t)u * d + k] : 0.0f;
+        float v = (u < N && k < d) ? W[(int64_t)u * d + k] : 0.0f;
+        if (v == 0.0f) v = 0.0f;
+        const unsigned bits = __float_as_uint(v);
+        const unsigned ex = bits & 0x7F800000u;
+        bad |= (bits >> 31) != 0u || ex == 0x7F800000u || (ex == 0u && bits != 0u);
+        tile[r][threadIdx.x] = v;
     }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += 8) {
         const int k = k0 + r, u = u0 + threadIdx.x;
@@ -106,8 +116,19 @@ template <> struct WtVec<true> {
     }
 };
 
+// Exact fp32 -> fp64 widening on the integer pipe, valid for +0 and positive
+// normal floats only (the host checks W^T holds nothing else): sign 0,
+// exponent e8 + 896, mantissa m23 << 29.  Used for half of the values so
+// that the F2F.F64.F32 pipe (~16/clk/SM) is not the only converter.
+__device__ __forceinline__ double widen_nonneg(float f) {
+    const unsigned b = __float_as_uint(f);
+    const unsigned hi = b ? (b >> 3) + 0x38000000u : 0u;
+    return __hiloint2double((int)hi, (int)(b << 29));
+}
+
 // Tile = 64 J units; lane l owns units u0 + VEC l + 32 VEC g + c (g < G, c < VEC).
-template <int J, bool F32>
+// ICV (fp32 storage only): groups g >= G/2 are widened on the integer pipe.
+template <int J, bool F32, bool ICV = false>
 __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseArgs a) {
     using L = WtVec<F32>;
     constexpr int VEC = L::VEC;
@@ -152,7 +173,18 @@ __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseA
 #pragma unroll
                 for (int e = 0; e < UN; ++e)
 #pragma unroll
-                    for (int g = 0; g < G; ++g) L::load(a.WT, (int64_t)k[e] * a.Np + lbase + 32 * VEC * g, w[e][g]);
+                    for (int g = 0; g < G; ++g) {
+                        if (ICV && g >= G / 2) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(
+                                static_cast<const float*>(a.WT) + (int64_t)k[e] * a.Np + lbase + 32 * VEC * g));
+                            w[e][g][0] = widen_nonneg(v.x);
+                            w[e][g][1] = widen_nonneg(v.y);
+                            w[e][g][2] = widen_nonneg(v.z);
+                            w[e][g][3] = widen_nonneg(v.w);
+                        } else {
+                            L::load(a.WT, (int64_t)k[e] * a.Np + lbase + 32 * VEC * g, w[e][g]);
+                        }
+                    }
 #pragma unroll
                 for (int e = 0; e < UN; ++e)
 #pragma unroll
@@ -197,10 +229,13 @@ __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseA
 int sparse_tile_units(int J) { return 64 * J; }
 int sparse_padded_units(int N, int J) { return (N + 64 * J - 1) / (64 * J) * (64 * J); }
 
-cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, double* wsq, cudaStream_t st) {
+cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, double* wsq, int* flag,
+                      cudaStream_t st) {
     dim3 g1((unsigned)((Np + 31) / 32), (unsigned)((d + 31) / 32));
-    if (f32) wt_kernel<float><<<g1, dim3(32, 8), 0, st>>>(W, N, d, Np, (float*)WT);
-    else wt_kernel<double><<<g1, dim3(32, 8), 0, st>>>(W, N, d, Np, (double*)WT);
+    cudaError_t e0 = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e0 != cudaSuccess) return e0;
+    if (f32) wt_kernel<float><<<g1, dim3(32, 8), 0, st>>>(W, N, d, Np, (float*)WT, flag);
+    else wt_kernel<double><<<g1, dim3(32, 8), 0, st>>>(W, N, d, Np, (double*)WT, flag);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     row_sqnorm_kernel<<<(N + 7) / 8, 256, 0, st>>>(W, N, d, wsq);
@@ -208,7 +243,7 @@ cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, 
 }
 
 cudaError_t launch_map_sparse(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t m,
-                              const void* WT, bool f32, const double* wsq, int N, int Np, int J,
+                              const void* WT, bool f32, bool icv, const double* wsq, int N, int Np, int J,
                               unsigned long long* keys, cudaStream_t st) {
     if (m <= 0) return cudaSuccess;
     const int tiles = Np / (64 * J);
@@ -216,6 +251,13 @@ cudaError_t launch_map_sparse(const int64_t* rowptr, const int32_t* col, const f
     if (const char* e = std::getenv("SOM_SPARSE_DPC")) docs_per_cta = std::max(16, std::atoi(e));
     SparseArgs a{rowptr, col, val, r0, m, WT, wsq, N, Np, docs_per_cta, keys};
     dim3 grid((unsigned)((m + docs_per_cta - 1) / docs_per_cta), (unsigned)tiles);
+    if (f32 && icv) {
+        switch (J) {
+            case 4: map_sparse_kernel<4, true, true><<<grid, SP_THREADS, 0, st>>>(a); return cudaGetLastError();
+            case 8: map_sparse_kernel<8, true, true><<<grid, SP_THREADS, 0, st>>>(a); return cudaGetLastError();
+            default: break;
+        }
+    }
     const int cfg = J * 2 + (f32 ? 1 : 0);
     switch (cfg) {
         case 2: map_sparse_kernel<1, false><<<grid, SP_THREADS, 0, st>>>(a); break;

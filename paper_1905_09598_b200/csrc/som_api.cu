@@ -99,7 +99,7 @@ struct som_ctx {
     DevBuf bS, bnum; // batch SOM: per-BMU sums S and H S (fp64, N x (d+1))
     DevBuf up, up2;  // upstream steps (TF-IDF / PCA scratch)
     DevBuf wt64;     // sparse mapping: W^T fp64 or fp32 (dim x Np) | |W|^2 fp64 (N)
-    bool wt_valid = false, wt_f32 = false;
+    bool wt_valid = false, wt_f32 = false, wt_nonneg = false;
     int wt_J = 0;
     // decay-table cache
     int64_t f_T = -1, f_t0 = -1, f_t1 = -1;
@@ -933,9 +933,14 @@ som_status ensure_wt(som_ctx* h, int J, bool f32, const void** WT, const double*
     const size_t plane = (f32 ? sizeof(float) : sizeof(double)) * (size_t)h->dim * np;
     *fresh = !h->wt_valid || h->wt_J != J || h->wt_f32 != f32;
     if (*fresh) {
-        CK(h->wt64.ensure(plane + sizeof(double) * (size_t)h->N, h->stream));
+        CK(h->wt64.ensure(plane + sizeof(double) * (size_t)h->N + 16, h->stream));
         char* base = (char*)h->wt64.p;
-        CK(launch_wt(h->W, h->N, h->dim, np, f32, base, (double*)(base + plane), h->stream));
+        int* flag = (int*)(base + plane + sizeof(double) * (size_t)h->N);
+        CK(launch_wt(h->W, h->N, h->dim, np, f32, base, (double*)(base + plane), flag, h->stream));
+        int bad = 1;
+        CK(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->wt_nonneg = bad == 0;
         h->wt_valid = true;
         h->wt_J = J;
         h->wt_f32 = f32;
@@ -982,6 +987,10 @@ som_status map_csr_dev(som_ctx* h, const CsrIn& csr, int64_t n, int32_t* b1, int
         int np = 0;
         som_status st = ensure_wt(h, J, f32, &WT, &wsq, &np, &fresh);
         if (st) return st;
+        // integer-pipe widening of half the values when W holds only +0 and
+        // positive normals (TF-IDF maps); SOM_SPARSE_ICV=0 disables it
+        bool icv = f32 && h->wt_nonneg && (J == 4 || J == 8);
+        if (const char* e = std::getenv("SOM_SPARSE_ICV")) icv = icv && std::atoi(e) != 0;
         if (fresh) *launches += 2;
         const int tiles = np / sparse_tile_units(J);
         // chunk so the partial keys stay <= 1 GiB
@@ -989,7 +998,7 @@ som_status map_csr_dev(som_ctx* h, const CsrIn& csr, int64_t n, int32_t* b1, int
         CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles * (size_t)chunk, h->stream));
         for (int64_t r0 = 0; r0 < n; r0 += chunk) {
             const int64_t m = std::min(chunk, n - r0);
-            CK(launch_map_sparse(csr.rowptr, csr.col, csr.val, r0, m, WT, f32, wsq, h->N, np, J,
+            CK(launch_map_sparse(csr.rowptr, csr.col, csr.val, r0, m, WT, f32, icv, wsq, h->N, np, J,
                                  (unsigned long long*)h->keys.p, h->stream));
             CK(launch_map_merge((const unsigned long long*)h->keys.p, tiles, m, b1 + r0, b2 ? b2 + r0 : nullptr,
                                 d2 ? d2 + r0 : nullptr, h->stream));

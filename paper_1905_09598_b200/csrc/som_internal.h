@@ -211,9 +211,13 @@ cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm
 // {1,2,4} x fp64, {2,4,8} x fp32.
 int sparse_tile_units(int J);
 int sparse_padded_units(int N, int J);
-cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, double* wsq, cudaStream_t st);
+// *flag (device int) is set when W holds a negative, subnormal, infinite or
+// NaN value; otherwise the fp32 variants may widen half of the values on the
+// integer pipe (icv).
+cudaError_t launch_wt(const float* W, int N, int d, int Np, bool f32, void* WT, double* wsq, int* flag,
+                      cudaStream_t st);
 cudaError_t launch_map_sparse(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t m,
-                              const void* WT, bool f32, const double* wsq, int N, int Np, int J,
+                              const void* WT, bool f32, bool icv, const double* wsq, int N, int Np, int J,
                               unsigned long long* keys, cudaStream_t st);
 
 // Batch SOM epoch pieces (batch.cu, R27): bucket documents by BMU (stable
