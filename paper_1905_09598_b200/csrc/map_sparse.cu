@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseA
     using L = WtVec<F32>;
     constexpr int VEC = L::VEC;
     constexpr int G = 64 * J / (32 * VEC);
-    constexpr int UN = (G * VEC > 8) ? 2 : 4;     // non-zeros in flight per iteration
+    // non-zeros in flight per iteration: fp32 storage keeps the raw float4 loads
+    // (4 registers each) and widens at use, so it affords twice as many
+    constexpr int UN = F32 ? 4 : ((G * VEC > 8) ? 2 : 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.y;
     const int u0 = tile * (64 * J);
@@ -169,28 +171,42 @@ __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseA
                     k[e] = __shfl_sync(0xffffffffu, kk, q + e);   // lanes >= cnt carry k = 0, v = 0
                     v[e] = __shfl_sync(0xffffffffu, vv, q + e);
                 }
-                double w[UN][G][VEC];
+                if constexpr (F32) {
+                    float4 raw[UN][G];
 #pragma unroll
-                for (int e = 0; e < UN; ++e)
+                    for (int e = 0; e < UN; ++e)
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        if (ICV && g >= G / 2) {
-                            const float4 v = __ldg(reinterpret_cast<const float4*>(
+                        for (int g = 0; g < G; ++g)
+                            raw[e][g] = __ldg(reinterpret_cast<const float4*>(
                                 static_cast<const float*>(a.WT) + (int64_t)k[e] * a.Np + lbase + 32 * VEC * g));
-                            w[e][g][0] = widen_nonneg(v.x);
-                            w[e][g][1] = widen_nonneg(v.y);
-                            w[e][g][2] = widen_nonneg(v.z);
-                            w[e][g][3] = widen_nonneg(v.w);
-                        } else {
-                            L::load(a.WT, (int64_t)k[e] * a.Np + lbase + 32 * VEC * g, w[e][g]);
+#pragma unroll
+                    for (int e = 0; e < UN; ++e)
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const float4 r = raw[e][g];
+                            double wv[4];
+                            if (ICV && g >= G / 2) {
+                                wv[0] = widen_nonneg(r.x); wv[1] = widen_nonneg(r.y);
+                                wv[2] = widen_nonneg(r.z); wv[3] = widen_nonneg(r.w);
+                            } else {
+                                wv[0] = (double)r.x; wv[1] = (double)r.y; wv[2] = (double)r.z; wv[3] = (double)r.w;
+                            }
+#pragma unroll
+                            for (int c = 0; c < VEC; ++c) acc[g][c] = fma(v[e], wv[c], acc[g][c]);
                         }
-                    }
+                } else {
+                    double w[UN][G][VEC];
 #pragma unroll
-                for (int e = 0; e < UN; ++e)
+                    for (int e = 0; e < UN; ++e)
 #pragma unroll
-                    for (int g = 0; g < G; ++g)
+                        for (int g = 0; g < G; ++g) L::load(a.WT, (int64_t)k[e] * a.Np + lbase + 32 * VEC * g, w[e][g]);
 #pragma unroll
-                        for (int c = 0; c < VEC; ++c) acc[g][c] = fma(v[e], w[e][g][c], acc[g][c]);
+                    for (int e = 0; e < UN; ++e)
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+#pragma unroll
+                            for (int c = 0; c < VEC; ++c) acc[g][c] = fma(v[e], w[e][g][c], acc[g][c]);
+                }
             }
         }
         xsq = warp_sum_f64(xsq);   // xor butterfly: every lane holds the same sum
