@@ -134,3 +134,30 @@ def test_upstream_chain_counts_to_trained_map(som):
     agree = np.mean(log == logo)
     assert agree >= 0.99, agree
     print(f" [chain: {rows}x{cols} map, {epochs} epochs, BMU agreement {agree:.4f}]", end="")
+
+
+def test_upstream_validation(som):
+    """Arguments are checked before any side effect (som.h conventions)."""
+    with som.SOM(2, 2, 5, 1) as m:
+        W0 = np.arange(20, dtype=np.float32).reshape(4, 5)
+        m.set_weights(W0)
+        rp = np.array([0, 2, 3], np.int64)
+        ci = np.array([0, 7, 1], np.int32)           # column 7 >= dim 5
+        cnt = np.ones(3, np.float32)
+        out = np.empty(3, np.float32)
+        with pytest.raises(som.SomError) as e:
+            som.som_tfidf_csr(m.h, rp, ci, cnt, 2, out)
+        assert e.value.status == som.SOM_EINVAL
+        with pytest.raises(som.SomError) as e:
+            m.pca_top2(np.ones((1, 5), np.float32))   # n = 1
+        assert e.value.status == som.SOM_EINVAL
+        with pytest.raises(som.SomError):
+            som.som_init_linear(m.h, np.zeros(5), np.zeros(5), np.zeros(5), float("nan"), 1.0)
+        assert np.array_equal(m.get_weights(), W0)
+        with pytest.raises(som.SomError):
+            som.som_map_geometry(0, 1.0, 1.0)
+        with pytest.raises(som.SomError):
+            som.som_map_geometry(10, -1.0, 1.0)
+        with pytest.raises(som.SomError) as e:
+            m.train_batch_csr(rp, ci, cnt, 2, 1, 1.0)  # malformed CSR: weights untouched
+        assert np.array_equal(m.get_weights(), W0)
