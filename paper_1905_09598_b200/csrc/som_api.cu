@@ -523,7 +523,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
             if (G < 1 || G > gmax) continue;
             const int R = small_rounds((h->NL + G - 1) / G, h->dim);
             double est = xchg_us(G) + 0.35 * R;   // ~0.35 us per round (tools/sweep_small.py, d = 64)
-            if (R > 4) est += 2.6 * 4.0 * (double)h->NL * h->dim / 12.0e6;   // read + ~60 % written, 12 TB/s L2
+            // streamed: read + ~60 % written per step at ~12 TB/s of L2 over 148 SMs, pro rata G
+            if (R > 4) est += 2.6 * 4.0 * (double)h->NL * h->dim / (12.0e6 * G / 148.0);
             if (est < best) { best = est; bestG = G; }
         }
         use_small = bestG > 0;
