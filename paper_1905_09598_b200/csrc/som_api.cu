@@ -568,6 +568,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
     a.trace = h->trace;
     a.trace_steps = h->trace ? h->trace_steps : 0;
+    a.trace_clk = 0;
+    if (const char* e = std::getenv("SOM_TRACE_CLOCK")) a.trace_clk = std::atoi(e) != 0;
     size_t smem = train_smem_bytes(a.S, a.dimp, 1);
     a.w_smem = smem <= (size_t)h->max_smem_optin;
     if (h->train_mode == SOM_TRAIN_W_SHARED && !a.w_smem)

@@ -39,6 +39,7 @@ struct TrainArgs {
     int x_vec4;                // 1: X rows are 16-byte aligned (d % 4 == 0)
     unsigned long long* trace; // nullable: [G][trace_steps][kTracePhases] globaltimer (ns) per CTA
     int trace_steps;
+    int trace_clk;             // 1: trace in SM cycles (clock64) instead of globaltimer ns
     // neuron sharding: this launch holds the N local units
     // l = 0..N-1 of global units u = rank + world * l; after the in-GPU
     // exchange, CTA 0 publishes the local winner into mail[p][t&1][rank] of
@@ -149,6 +150,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+// trace clock: %globaltimer (ns, comparable across SMs, coarse) or, with
+// SOM_TRACE_CLOCK=1, the SM cycle counter (fine, per-SM only)
+__device__ __forceinline__ unsigned long long trace_now(int clk) {
+    if (clk) {
+        unsigned long long c;
+        asm volatile("mov.u64 %0, %clock64;" : "=l"(c));
+        return c;
+    }
+    return globaltimer_ns();
 }
 
 size_t train_smem_bytes(int S, int dimp, int w_smem);

@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
         unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
         if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
-        if (tr) tr[0] = globaltimer_ns();
+        if (tr) tr[0] = trace_now(a.trace_clk);
         const float4* xc4 = reinterpret_cast<const float4*>(xbuf + (size_t)(t & 1) * a.dimp);         // x_t
         const float4* xp4 = reinterpret_cast<const float4*>(xbuf + (size_t)((t + 1) & 1) * a.dimp);   // x_{t-1}
         const int nup = s_nup;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
             acc = warp_sum_f64(acc);
             if (lane == 0) dsp[s] = wns[s] + acc;
         }
-        if (tr) tr[1] = globaltimer_ns();
+        if (tr) tr[1] = trace_now(a.trace_clk);
 
         // ---- dense path: pending Eq. 1 update + distance + new |w|^2
         for (int i = 0; i < nup; ++i) {
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
             for (int j = 0; j < KJ; ++j) cur[j] = nxt[j];
         }
         __syncthreads();   // (A) pass done: x_{t-1} free, partials complete
-        if (tr) tr[2] = globaltimer_ns();
+        if (tr) tr[2] = trace_now(a.trace_clk);
 
         // x_{t-1}'s dense slot -> zeros; x_{t+1}'s list in flight; bounds of x_{t+2}
         {
@@ -286,14 +286,14 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
                 best = umin64(best, make_key((float)tot, global_unit(a, uid[s])));
             }
             best = warp_min_u64(best);
-            if (tr) tr[3] = globaltimer_ns();
+            if (tr) tr[3] = trace_now(a.trace_clk);
             xchg_publish(a, best, t, b, lane);
-            if (tr) tr[4] = globaltimer_ns();
+            if (tr) tr[4] = trace_now(a.trace_clk);
             const double f = a.f_tab[t - a.t0];
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
             if (stop && lane == 0) s_abort = 1;
-            if (tr) tr[5] = globaltimer_ns();
+            if (tr) tr[5] = trace_now(a.trace_clk);
             const int c = key_unit(gmin);
             if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
             const double alpha = a.alpha0 * f;
@@ -323,14 +323,14 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
                 n_no += __popc(mn);
             }
             if (lane == 0) s_nup = n_up;
-            if (tr) tr[6] = globaltimer_ns();
+            if (tr) tr[6] = trace_now(a.trace_clk);
         }
         cp_async_wait_all();
         __syncthreads();   // (B) list of x_{t+1} landed, x_{t-1} slot zeroed
         if (s_abort) break;
         scatter(t + 1);
         __syncthreads();   // (C) x_{t+1} dense
-        if (tr) tr[7] = globaltimer_ns();
+        if (tr) tr[7] = trace_now(a.trace_clk);
     }
 
     // flush the update of the last step (x_{t1-1} in dense slot (t1-1) & 1)
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
         if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
-        if (tr) tr[0] = globaltimer_ns();
+        if (tr) tr[0] = trace_now(a.trace_clk);
         const int nup = s_nup;
 
         // ---- dense pass over the pending update's rows (ring, issued by
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             }
         }
         q += nup;   // the last row's barrier is barrier A (keys need every partial)
-        if (tr) tr[1] = globaltimer_ns();
+        if (tr) tr[1] = trace_now(a.trace_clk);
 
         const double f = a.f_tab[t - a.t0];
         const double alpha = a.alpha0 * f;
@@ -568,12 +568,12 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
                 best = umin64(best, make_key((float)tot, global_unit(a, uid[s])));
             }
             best = warp_min_u64(best);
-            if (tr) tr[2] = globaltimer_ns();
+            if (tr) tr[2] = trace_now(a.trace_clk);
             xchg_publish(a, best, t, b, lane);
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
             if (stop && lane == 0) s_abort = 1;
-            if (tr) tr[3] = globaltimer_ns();
+            if (tr) tr[3] = trace_now(a.trace_clk);
             const int c = key_unit(gmin);
             if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
             int n_up = 0, n_no = 0;
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
                     }
                 }
             }
-            if (tr) tr[4] = globaltimer_ns();
+            if (tr) tr[4] = trace_now(a.trace_clk);
         } else {
             // warps 1-15: list of x_{t+2}, bounds of x_{t+3}, and the
             // speculative sparse sums of step t+1 (skipped when the radius
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         }
         cp_async_wait_all();
         __syncthreads();   // (B) lists, ring issue, sparse sums of t+1
-        if (tr) tr[5] = globaltimer_ns();
+        if (tr) tr[5] = trace_now(a.trace_clk);
         if (s_abort) break;
         scatter(t + 1);
         __syncthreads();   // (C) x_{t+1} in xs
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             }
             xd[j][0] = xc[j].x; xd[j][1] = xc[j].y; xd[j][2] = xc[j].z; xd[j][3] = xc[j].w;
         }
-        if (tr) tr[6] = globaltimer_ns();
+        if (tr) tr[6] = trace_now(a.trace_clk);
     }
 
     // flush the update of the last step (x_{t1-1} is now in xp)

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
         if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
-#define TRACE(p) do { if (tr) tr[p] = globaltimer_ns(); } while (0)
+#define TRACE(p) do { if (tr) tr[p] = trace_now(a.trace_clk); } while (0)
         TRACE(0);
 
         // ---- fused pass on registers: pending update (t-1), then D_u(x_t)

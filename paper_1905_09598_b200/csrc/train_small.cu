@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_small_kernel(const TrainArgs 
         unsigned long long* tr = nullptr;
         if (a.trace && (threadIdx.x == 0 || threadIdx.x == 32) && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
-#define TRACE(p) do { if (tr) tr[p] = globaltimer_ns(); } while (0)
+#define TRACE(p) do { if (tr) tr[p] = trace_now(a.trace_clk); } while (0)
         if (threadIdx.x == 0) TRACE(0);
         const float4* xp4 = ring4 + (size_t)((t + 2) % 3) * d4;   // x_{t-1}
         // ---- fused pass: pending update (t-1), then D_u(x_t), per-lane min key
