@@ -81,3 +81,34 @@ def test_c5_full_size_mapping(corpus):
     assert np.all(b1 >= 0) and np.all(b1 < 10000) and np.all(b2 != b1)
     print(f" [c5 full size: {N_DOCS} docs in {ms:.0f} ms = {N_DOCS / ms * 1e3 / 1e6:.2f} M docs/s, "
           f"{launches} launches, QE {qe:.6f}, TE {te:.4f}]", end="")
+
+
+def test_c3_full_schedule_tail():
+    """BASELINE.json configs[2] (c3: 50x50 hex, 50,000 x 10,000 TF-IDF,
+    10 epochs = 500,000 steps) trained on the GPU in the bench's launch
+    configuration; the last 100 steps (smallest radius, alpha near alpha0/100)
+    are re-run by the oracle from the GPU's weights at step 499,900 (the
+    t-range resume is exact, tests/test_gpu_parity.py) and must give the same
+    BMU log and weights; the final QE must beat the initial codebook's."""
+    from paper_1905_09598_b200 import som
+    from synth import init_rows
+    C = bank_corpus(50000, 10000, seed=3)
+    X = C.dense()
+    W0 = init_rows(X, 2500, 1003)
+    T, t0 = 500000, 499900
+    with som.SOM(50, 50, 10000, 1) as m:
+        m.set_weights(W0)
+        qe0, _ = m.errors(X)
+        m.train_online(X, epochs=10, alpha0=0.1, sigma0=25.0, seed=3, t_end=t0)
+        ms, units, _ = som.som_last_stats(m.h)
+        Wt0 = m.get_weights()
+        log = np.empty(T - t0, np.int32)
+        m.train_online(X, epochs=10, alpha0=0.1, sigma0=25.0, seed=3, t_begin=t0, bmu_log=log)
+        W = m.get_weights()
+        qe1, te1 = m.errors(X)
+    Wo, logo = oracle.train_online(Wt0, 50, 50, 1, X, 10, 0.1, 25.0, 3, t_begin=t0)
+    assert np.array_equal(log, logo)
+    assert np.abs(W.astype(np.float64) - Wo).max() <= 1e-4
+    assert qe1 < qe0
+    print(f" [c3 full schedule: {units} steps in {ms / 1e3:.2f} s = {1e3 * ms / units:.1f} us/step, "
+          f"QE {qe0:.4f} -> {qe1:.4f}, TE {te1:.4f}]", end="")
