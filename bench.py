@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--c3-steps", type=int, default=20000, help="steps of the c3 training leg (0 = skip)")
     p.add_argument("--table3-steps", type=int, default=20000, help="steps per map of the Table 3 leg (0 = skip)")
     p.add_argument("--batch-epochs", type=int, default=10, help="epochs of the batch-SOM leg (0 = skip)")
+    p.add_argument("--c4-steps", type=int, default=2000, help="steps of the c4 (neuron-sharded at N > 1) leg (0 = skip)")
+    p.add_argument("--c4-docs", type=int, default=20000, help="documents of the c4 leg (replicated on every rank)")
     return p.parse_args()
 
 
@@ -296,6 +298,64 @@ def batch_leg(som, torch, args, local, seed):
                     "whole epoch time (mapping, bucketing, sums included); tiles outside the cutoff are skipped"}
 
 
+def c4_leg(som, torch, args, local, rank, world):
+    """c4 (BASELINE.json configs[3]: 100x100 hex map, 20,000 terms) online
+    training, the first --c4-steps steps.  At N > 1 the map is neuron-sharded
+    over the ranks (dist.ShardedSOM: units u = r + P l, X replicated, the
+    per-step winner exchanged inside the training kernel through peer-memory
+    mailboxes over NVLink); at N = 1 the same steps on one GPU.  Failures are
+    contained: every rank reports its status through an all-reduce and the
+    leg returns an error entry instead of stopping the bench."""
+    import torch.distributed as dist
+    rows = cols = 100
+    d, n, steps = 20000, args.c4_docs, args.c4_steps
+    C = bank_corpus(n, d, seed=args.seed + 400)                  # identical on every rank
+    X = torch.from_numpy(C.dense()).cuda(local)
+    from synth import init_rows
+    W0 = torch.from_numpy(init_rows(C.dense(), rows * cols, args.seed + 401) if n >= rows * cols else
+                          (0.5 * bank_corpus(rows * cols, d, seed=args.seed + 402).dense()
+                           + 0.5 * C.dense().mean(0)).astype(np.float32)).cuda(local)
+    ok = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ms, err, chk = 0.0, "", 0.0
+    try:
+        log = torch.empty(steps, dtype=torch.int32, device="cuda")
+        if world > 1:
+            from paper_1905_09598_b200.dist import ShardedSOM
+            sm = ShardedSOM(rows, cols, d, 1, rank, world, device=local)
+            sm.set_weights(W0)
+            dist.barrier()
+            som.som_train_online(sm.h, X, n, 2, ALPHA0, 50.0, None, args.seed, 0, steps, log)
+            ms, _, _ = som.som_last_stats(sm.h)
+            g, k = som.som_last_train_config(sm.h)
+            sm.close()
+        else:
+            with som.SOM(rows, cols, d, 1, device=local) as m1:
+                m1.set_weights(W0)
+                som.som_train_online(m1.h, X, n, 2, ALPHA0, 50.0, None, args.seed, 0, steps, log)
+                ms, _, _ = som.som_last_stats(m1.h)
+                g, k = som.som_last_train_config(m1.h)
+        lg = log.cpu().numpy().astype(np.float64)
+        chk = float((lg * (1 + np.arange(steps) % 977)).sum())
+    except Exception as e:      # contained: reported below, never left hanging in a collective
+        ok[0] = 1.0
+        err = str(e)[:200]
+        g, k = 0, -1
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+    if ok.item() > 0:
+        return {"workload": "c4 neuron-sharded training", "error": err or "failed on another rank"}
+    t = torch.tensor([ms, chk, -chk], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, consistent = float(t[0]), bool(float(t[1]) == -float(t[2]))
+    return {"workload": f"c4: 100x100 hex, 20,000 terms, {n} docs replicated, steps [0, {steps}) of 2 epochs, "
+                        f"{'neuron-sharded over ' + str(world) + ' GPUs (in-kernel NVLink winner exchange)' if world > 1 else 'one GPU'}",
+            "samples_per_s": steps / (ms_max / 1000.0), "us_per_step": 1000.0 * ms_max / steps,
+            "units_per_gpu": (rows * cols + world - 1) // world, "grid": g, "kernel": k,
+            "scaling": "strong (one map, units split over the ranks)",
+            "bmu_log_identical_on_all_ranks": consistent}
+
+
 TABLE3_PAPER_S = {16: 34.25, 32: 32.81, 64: 33.37, 128: 38.40, 256: 111.03, 512: 431.38}   # P:304-305
 
 
@@ -523,6 +583,7 @@ def run_b200(args, rank, world, local):
     train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
     table3 = table3_leg(som, torch, args, local, seed) if args.table3_steps > 0 else None
     batch = batch_leg(som, torch, args, local, seed) if args.batch_epochs > 0 else None
+    c4 = c4_leg(som, torch, args, local, rank, world) if args.c4_steps > 0 else None
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -561,6 +622,7 @@ def run_b200(args, rank, world, local):
         "train_c3": train_c3,
         "table3": table3,
         "batch_som": batch,
+        "train_c4": c4,
         "roofline": {"bound": "alu", "kernel": f"{kname}, G={g_used}", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
