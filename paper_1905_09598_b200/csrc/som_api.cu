@@ -639,12 +639,19 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // persisting access-policy window (random X rows stream past it), undone
     // after the launch so the caller's stream is left as it was.
     bool l2_window = false;
-    if (!use_reg && !a.w_smem && (!use_small || small_rounds(a.S, h->dim) > 4)) {
+    const char* nowin = std::getenv("SOM_NO_L2_WINDOW");
+    if (!(nowin && std::atoi(nowin)) && !use_reg && !a.w_smem && (!use_small || small_rounds(a.S, h->dim) > 4)) {
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
         const size_t wbytes = sizeof(float) * (size_t)h->NL * h->dim;
-        if (max_persist > 0 && max_window > 0) {
+        int l2_bytes = 0;
+        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, h->device);
+        // only for maps that fit the L2: for a map several times the L2 (c4 on
+        // one GPU, 800 MB) the persisting lines of the window crowd out the
+        // streamed rest of W and the row writes (measured 664 -> 263 us/step
+        // without it)
+        if (max_persist > 0 && max_window > 0 && wbytes <= (size_t)l2_bytes) {
             const size_t win = std::min(wbytes, (size_t)max_window);
             const size_t keep = std::min(win, (size_t)max_persist);
             if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep) == cudaSuccess) {
