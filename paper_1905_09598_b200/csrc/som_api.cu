@@ -673,11 +673,10 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
-    if (l2_window) {
+    if (l2_window) {   // later launches on the caller's stream get no window
         cudaStreamAttrValue at{};
         at.accessPolicyWindow.num_bytes = 0;
         cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at);
-        cudaCtxResetPersistingL2Cache();
         cudaGetLastError();
     }
     h->last_grid = a.G;
@@ -685,6 +684,11 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (l2_window) {   // the kernel is done: demote its persisting lines and release the set-aside L2
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+    }
     unsigned abort_flag = 0;
     CK(cudaMemcpyAsync(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
