@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsom.so")
+LIB_PATH = os.environ.get("SOM_LIB", os.path.join(_HERE, "libsom.so"))   # SOM_LIB: A/B a second build
 
 SOM_OK, SOM_EINVAL, SOM_EDIM, SOM_EEMPTY, SOM_ENOMEM, SOM_ECUDA, SOM_ENCCL, SOM_ESTATE, SOM_EUNSUPPORTED = range(9)
 SOM_RECT, SOM_HEX = 0, 1
