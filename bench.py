@@ -412,10 +412,25 @@ def train_c3_leg(som, torch, args, local, seed):
     gbps = algo / (ms / 1000.0) / 1e9
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         hbm = float(json.load(f)["hbm_gbs"])
+    # late window (radius near sigma_min: few units updated): the dense kernel
+    # still reads all of W per step; the CSR kernel's sparse distance reads
+    # only the non-zero columns
+    late = {}
+    t0 = T - steps
+    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
+    for name, csr in (("dense", False), ("csr", True)):
+        som.som_init_random(mm.h, X, n, seed + 1300)
+        if csr:
+            som.som_train_online_csr(mm.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, t0, T, None)
+        else:
+            som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, t0, T, None)
+        lms, _, _ = som.som_last_stats(mm.h)
+        late[name] = {"us_per_step": 1000.0 * lms / steps, "kernel": som.som_last_train_config(mm.h)[1]}
     mm.close()
     return {"workload": f"c3: {cfg['rows']}x{cfg['cols']} hex, {n} x {d}, steps [0, {steps}) of T = {T}",
             "samples_per_s": steps / (ms / 1000.0), "us_per_step": 1000.0 * ms / steps,
             "mean_updated_units": float(H.mean()),
+            "late_window": {"steps": f"[{t0}, {T})", **late},
             "roofline": {"bound": "hbm", "kernel": f"som_train_glb_kernel (kernel id {kern}), G={g}",
                          "achieved": gbps, "peak": hbm, "unit": "GB/s", "frac": gbps / hbm,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
