@@ -124,13 +124,32 @@ struct GemmArgs {
     double two_s2, r2;
 };
 
+// K steps whose lattice-row span lies inside the cutoff (block-uniform)
+__device__ __forceinline__ bool gemm_step_live(const GemmArgs& a, int c0, int ur0, int ur1) {
+    const int clast = min(a.N, c0 + GK) - 1;
+    const int cr0 = c0 / a.cols, cr1 = clast / a.cols;
+    const int gap = max(0, max(ur0, cr0) - min(ur1, cr1));   // smallest |di| between the tiles
+    const double g2min = a.topo == 0 ? (double)gap * gap : 0.75 * ((double)gap * gap);
+    return g2min <= a.r2;
+}
+
+__device__ __forceinline__ int gemm_next_live(const GemmArgs& a, int c0, int ur0, int ur1) {
+    while (c0 < a.N && !gemm_step_live(a, c0, ur0, ur1)) c0 += GK;
+    return c0;
+}
+
+// Double-buffered: while the FMAs of step k run on buffer k&1, the S tile of
+// the next live step streams into the other buffer with cp.async and its h
+// tile is generated there; one barrier per step.  Lattice coordinates of all
+// units come from a packed (i << 16 | j) table in shared memory.
 __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
-    __shared__ double hs[GK][GM + 1];
-    __shared__ double ss[GK][GN];
-    extern __shared__ double tabs[];   // Er[rows] | Ec[W2]
+    extern __shared__ __align__(16) double dyn[];
+    double (*hs)[GK][GM + 1] = reinterpret_cast<double (*)[GK][GM + 1]>(dyn);                 // [2]
+    double (*ss)[GK][GN] = reinterpret_cast<double (*)[GK][GN]>(dyn + 2 * GK * (GM + 1));     // [2]
     const int W2 = a.topo == 0 ? a.cols : 2 * a.cols;
-    double* er = tabs;
-    double* ec = tabs + a.rows;
+    double* er = dyn + 2 * GK * (GM + 1) + 2 * GK * GN;
+    double* ec = er + a.rows;
+    int* pij = reinterpret_cast<int*>(ec + W2);                                              // [N]
     for (int e = threadIdx.x; e < a.rows + W2; e += GT) {
         if (e < a.rows) {
             const double di = (double)e;
@@ -140,45 +159,43 @@ __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
             ec[e - a.rows] = exp(-(a.topo == 0 ? dx * dx : 0.25 * (dx * dx)) / a.two_s2);
         }
     }
+    for (int u = threadIdx.x; u < a.N; u += GT) {
+        const int i = u / a.cols;
+        pij[u] = (i << 16) | (u - i * a.cols);
+    }
     __syncthreads();
 
     const int u0 = blockIdx.y * GM, k0 = blockIdx.x * GN;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    // lattice coordinates of the tile's units (fixed) and of each K step's units
-    __shared__ int ui[GM], uj[GM], ci[GK], cj[GK];
-    for (int t = threadIdx.x; t < GM; t += GT) {
-        const int u = min(u0 + t, a.N - 1);
-        ui[t] = u / a.cols;
-        uj[t] = u - ui[t] * a.cols;
-    }
     double acc[TI][TJ];
 #pragma unroll
     for (int i = 0; i < TI; ++i)
 #pragma unroll
         for (int j = 0; j < TJ; ++j) acc[i][j] = 0.0;
-    // lattice rows spanned by this unit tile (for the cutoff skip)
     const int ulast = min(a.N, u0 + GM) - 1;
     const int ur0 = u0 / a.cols, ur1 = ulast / a.cols;
 
-    for (int c0 = 0; c0 < a.N; c0 += GK) {
-        const int clast = min(a.N, c0 + GK) - 1;
-        const int cr0 = c0 / a.cols, cr1 = clast / a.cols;
-        const int gap = max(0, max(ur0, cr0) - min(ur1, cr1));   // smallest |di| between the tiles
-        const double g2min = a.topo == 0 ? (double)gap * gap : 0.75 * ((double)gap * gap);
-        if (g2min > a.r2) continue;   // block-uniform: no pair of the tiles is inside the cutoff
-        __syncthreads();
-        if (threadIdx.x < GK) {
-            const int c = min(c0 + (int)threadIdx.x, a.N - 1);
-            ci[threadIdx.x] = c / a.cols;
-            cj[threadIdx.x] = c - ci[threadIdx.x] * a.cols;
+    // stage step c0 into buffer q: S tile by cp.async (zero-filled edges), h tile computed
+    auto stage = [&](int c0, int q) {
+        for (int e = threadIdx.x; e < GK * GN / 2; e += GT) {      // 16-byte pieces
+            const int cc = e / (GN / 2), kk = 2 * (e - cc * (GN / 2));
+            const int c = c0 + cc, k = k0 + kk;
+            double* dst = &ss[q][cc][kk];
+            if (c < a.N && k + 1 < a.dp && (((size_t)c * a.dp + k) & 1) == 0) {
+                cp_async16(dst, a.S + (size_t)c * a.dp + k);
+            } else {
+                dst[0] = (c < a.N && k < a.dp) ? a.S[(size_t)c * a.dp + k] : 0.0;
+                dst[1] = (c < a.N && k + 1 < a.dp) ? a.S[(size_t)c * a.dp + k + 1] : 0.0;
+            }
         }
-        __syncthreads();
+        cp_async_commit();
         for (int e = threadIdx.x; e < GK * GM; e += GT) {
             const int cc = e / GM, uu = e - cc * GM;
             const int u = u0 + uu, c = c0 + cc;
             double h = 0.0;
             if (u < a.N && c < a.N) {
-                const int iu = ui[uu], ju = uj[uu], ic = ci[cc], jc = cj[cc];
+                const int pu = pij[u], pc = pij[c];
+                const int iu = pu >> 16, ju = pu & 0xFFFF, ic = pc >> 16, jc = pc & 0xFFFF;
                 const int di = abs(iu - ic);
                 int dx;
                 double g2;
@@ -191,26 +208,34 @@ __global__ void __launch_bounds__(GT) batch_gemm_kernel(const GemmArgs a) {
                 }
                 if (g2 <= a.r2) h = er[di] * ec[dx];
             }
-            hs[cc][uu] = h;
+            hs[q][cc][uu] = h;
         }
-        for (int e = threadIdx.x; e < GK * GN; e += GT) {
-            const int cc = e / GN, kk = e - cc * GN;
-            const int c = c0 + cc, k = k0 + kk;
-            ss[cc][kk] = (c < a.N && k < a.dp) ? a.S[(size_t)c * a.dp + k] : 0.0;
-        }
-        __syncthreads();
+    };
+
+    int c0 = gemm_next_live(a, 0, ur0, ur1);
+    int q = 0;
+    if (c0 < a.N) stage(c0, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    while (c0 < a.N) {
+        const int cn = gemm_next_live(a, c0 + GK, ur0, ur1);
+        if (cn < a.N) stage(cn, q ^ 1);                         // next step into the other buffer
 #pragma unroll
         for (int cc = 0; cc < GK; ++cc) {
             double hv[TI], sv[TJ];
 #pragma unroll
-            for (int i = 0; i < TI; ++i) hv[i] = hs[cc][ty + 16 * i];
+            for (int i = 0; i < TI; ++i) hv[i] = hs[q][cc][ty + 16 * i];
 #pragma unroll
-            for (int j = 0; j < TJ; ++j) sv[j] = ss[cc][tx + 16 * j];
+            for (int j = 0; j < TJ; ++j) sv[j] = ss[q][cc][tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < TI; ++i)
 #pragma unroll
                 for (int j = 0; j < TJ; ++j) acc[i][j] = fma(hv[i], sv[j], acc[i][j]);
         }
+        cp_async_wait_all();
+        __syncthreads();
+        c0 = cn;
+        q ^= 1;
     }
 #pragma unroll
     for (int i = 0; i < TI; ++i) {
@@ -316,11 +341,12 @@ cudaError_t launch_batch_accumulate_csr(const int64_t* rowptr, const int32_t* co
 cudaError_t launch_batch_update(const double* S, double* num, int N, int d, int rows, int cols, int topo,
                                 double sigma, double r2, float* W, cudaStream_t st) {
     GemmArgs a{S, num, N, d + 1, rows, cols, topo, 2.0 * sigma * sigma, r2};
-    const size_t tab = sizeof(double) * ((size_t)rows + (topo == 0 ? cols : 2 * cols));
-    cudaError_t e = cudaFuncSetAttribute(batch_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
+    const size_t dyn = sizeof(double) * (2 * (size_t)GK * (GM + 1) + 2 * (size_t)GK * GN + (size_t)rows +
+                                         (topo == 0 ? cols : 2 * cols)) + sizeof(int) * (size_t)N;
+    cudaError_t e = cudaFuncSetAttribute(batch_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((d + 1 + GN - 1) / GN), (unsigned)((N + GM - 1) / GM));
-    batch_gemm_kernel<<<grid, GT, tab, st>>>(a);
+    batch_gemm_kernel<<<grid, GT, dyn, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int blocks = (int)std::min<int64_t>(((int64_t)N * d + 255) / 256, 148 * 16);

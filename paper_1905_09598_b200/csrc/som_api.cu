@@ -1129,6 +1129,7 @@ som_status train_batch_impl(som_ctx* h, const float* Xd, const CsrIn* csr, int64
     if (!(sd.sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
     if (!(sd.cutoff >= 0.0 && sd.cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
     if (n > INT32_MAX) return fail(SOM_EUNSUPPORTED, "batch SOM: n >= 2^31 rows");
+    if (h->N > 32768) return fail(SOM_EUNSUPPORTED, "batch SOM: more than 32768 units (N x N contraction)");
     const int N = h->N, d = h->dim;
     const size_t tb = batch_sort_temp_bytes(n, N);
     const size_t ints = 4 * (size_t)n + 2 * (size_t)N;
