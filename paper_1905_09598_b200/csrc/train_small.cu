@@ -40,7 +40,7 @@ namespace {
 
 constexpr int NT = kTrainThreads;
 constexpr int NW = kTrainWarps;
-constexpr int SC = 4;     // float4 chunks per lane: a lane group of L lanes covers 16 L floats
+constexpr int kSC = 4;    // float4 chunks per lane of the default layout: L lanes cover 16 L floats
 
 __device__ __forceinline__ float4 eq1s(float h, float4 w, float4 x) {
     // Eq. 1 per element: w + h (x - w) as fmaf(h, RN(x - w), w)  (R11)
@@ -83,7 +83,9 @@ __device__ __forceinline__ float h_of(const TrainArgs& a, int iu, int ju, int ic
     return (float)(sc.alpha * (er[di] * ec[dx]));
 }
 
-template <int L, int R, bool GLB>
+// SC float4 chunks per lane (kSC by default; 2 or 1 spread a CTA's units
+// over more lanes when they all fit one round: shorter per-lane chains)
+template <int L, int SC, int R, bool GLB>
 __global__ void __launch_bounds__(NT, 1) som_train_small_kernel(const TrainArgs a) {
     constexpr int GPW = 32 / L;            // units per warp per round
     constexpr int UPR = NW * GPW;          // units per CTA per round
@@ -312,32 +314,38 @@ size_t small_smem_bytes(const TrainArgs& a) {
     return sizeof(float) * 3 * (size_t)a.dimp + sizeof(double) * ((size_t)a.dimp + a.rows + W2);
 }
 
-template <int L, int R, bool GLB>
+template <int L, int SC, int R, bool GLB>
 cudaError_t launch_small_one(const TrainArgs& a, cudaStream_t st) {
     const size_t smem = small_smem_bytes(a);
-    cudaError_t e = cudaFuncSetAttribute(som_train_small_kernel<L, R, GLB>,
+    cudaError_t e = cudaFuncSetAttribute(som_train_small_kernel<L, SC, R, GLB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     TrainArgs args = a;
     void* params[] = {&args};
-    return launch_persistent((const void*)som_train_small_kernel<L, R, GLB>, a, NT, smem, params, st);
+    return launch_persistent((const void*)som_train_small_kernel<L, SC, R, GLB>, a, NT, smem, params, st);
 }
 
 template <int L>
 cudaError_t launch_small_L(const TrainArgs& a, int rounds, cudaStream_t st) {
-    if (rounds <= 1) return launch_small_one<L, 1, false>(a, st);
-    if (rounds <= 2) return launch_small_one<L, 2, false>(a, st);
-    if (rounds <= 4) return launch_small_one<L, 4, false>(a, st);
-    return launch_small_one<L, 1, true>(a, st);
+    if (rounds <= 1) {
+        // one round: widen the lane groups while the CTA's units still fit it
+        const int S = a.S;
+        if (L * 4 <= 32 && S <= kTrainWarps * (32 / (L * 4))) return launch_small_one<(L * 4 <= 32 ? L * 4 : 32), 1, 1, false>(a, st);
+        if (L * 2 <= 32 && S <= kTrainWarps * (32 / (L * 2))) return launch_small_one<(L * 2 <= 32 ? L * 2 : 32), 2, 1, false>(a, st);
+        return launch_small_one<L, kSC, 1, false>(a, st);
+    }
+    if (rounds <= 2) return launch_small_one<L, kSC, 2, false>(a, st);
+    if (rounds <= 4) return launch_small_one<L, kSC, 4, false>(a, st);
+    return launch_small_one<L, kSC, 1, true>(a, st);
 }
 
 }  // namespace
 
-// lanes per unit: SC = 4 float4 chunks per lane, L a power of two
+// lanes per unit of the default layout: kSC float4 chunks per lane, L a power of two
 int small_lanes(int dim) {
     const int d4 = (dim + 3) / 4;
     int L = 1;
-    while (L * SC < d4) L <<= 1;
+    while (L * kSC < d4) L <<= 1;
     return L;
 }
 
