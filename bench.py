@@ -317,12 +317,23 @@ def c4_leg(som, torch, args, local, rank, world):
                            + 0.5 * C.dense().mean(0)).astype(np.float32)).cuda(local)
     ok = torch.zeros(1, dtype=torch.float64, device="cuda")
     ms, err, chk = 0.0, "", 0.0
-    try:
-        log = torch.empty(steps, dtype=torch.int32, device="cuda")
-        if world > 1:
+    sm = None
+    if world > 1:
+        # set-up (IPC mailboxes) and training each end in an all-reduced
+        # status, so a rank that fails never leaves the others in a collective
+        try:
             from paper_1905_09598_b200.dist import ShardedSOM
             sm = ShardedSOM(rows, cols, d, 1, rank, world, device=local)
             sm.set_weights(W0)
+        except Exception as e:
+            ok[0] = 1.0
+            err = "setup: " + str(e)[:200]
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+        if ok.item() > 0:
+            return {"workload": "c4 neuron-sharded training", "error": err or "set-up failed on another rank"}
+    try:
+        log = torch.empty(steps, dtype=torch.int32, device="cuda")
+        if world > 1:
             dist.barrier()
             som.som_train_online(sm.h, X, n, 2, ALPHA0, 50.0, None, args.seed, 0, steps, log)
             ms, _, _ = som.som_last_stats(sm.h)
