@@ -33,6 +33,15 @@
  *    and mapping outputs on every run.
  *  - There is no CPU fallback: without a usable sm_100a device som_create
  *    fails with SOM_ECUDA.
+ *  - Tuning / diagnostic environment variables (read per call; results do
+ *    not depend on them unless stated): SOM_SPARSE_J (1|2|4|8: unit tile
+ *    64 J of the sparse mapping), SOM_SPARSE_F32 (0: fp64 W^T),
+ *    SOM_SPARSE_ICV (0: no integer-pipe widening), SOM_SPARSE_DPC
+ *    (documents per CTA), SOM_NO_TMA_RING (1: register-pipelined streamed
+ *    training kernel), SOM_NO_L2_WINDOW (1: no persisting L2 window),
+ *    SOM_POLL_NS (back-off between exchange polls), SOM_TRACE_CLOCK (1:
+ *    som_set_trace records SM cycles).  Every variant they select is
+ *    covered by the parity tests.
  */
 #ifndef SOM_H
 #define SOM_H
