@@ -298,6 +298,56 @@ def batch_leg(som, torch, args, local, seed):
                     "whole epoch time (mapping, bucketing, sums included); tiles outside the cutoff are skipped"}
 
 
+def exchange_probe(som, torch, args, local, rank, world):
+    """Per-step cost of the winner exchange alone: a map of 16 units per GPU
+    with d = 64 (negligible work per step), 20,000 steps; at N > 1 neuron-
+    sharded (in-GPU all-gather + cross-GPU mailbox exchange over NVLink),
+    at N = 1 the in-GPU all-gather only.  The difference is the cross-GPU
+    latency the sharded training pays every step."""
+    import torch.distributed as dist
+    from synth import uniform_matrix
+    side_c = 16
+    steps, n = 20000, 2000
+    X = torch.from_numpy(uniform_matrix(n, 64, args.seed + 700)).cuda(local)
+    W0 = torch.from_numpy(uniform_matrix(world * side_c, 64, args.seed + 701)).cuda(local)
+    ok = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ms = 0.0
+    sm = None
+    try:
+        if world > 1:
+            from paper_1905_09598_b200.dist import ShardedSOM
+            sm = ShardedSOM(world, side_c, 64, 1, rank, world, device=local)
+            sm.set_weights(W0)
+    except Exception:
+        ok[0] = 1.0
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+        if ok.item() > 0:
+            return {"error": "set-up failed"}
+    try:
+        if world > 1:
+            dist.barrier()
+            som.som_train_online(sm.h, X, n, 10, ALPHA0, 8.0, None, args.seed, 0, steps, None)
+            ms, _, _ = som.som_last_stats(sm.h)
+            sm.close()
+        else:
+            with som.SOM(1, side_c, 64, 1, device=local) as m1:
+                m1.set_weights(W0)
+                som.som_train_online(m1.h, X, n, 10, ALPHA0, 8.0, None, args.seed, 0, steps, None)
+                ms, _, _ = som.som_last_stats(m1.h)
+    except Exception:
+        ok[0] = 1.0
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+    if ok.item() > 0:
+        return {"error": "exchange probe failed"}
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"us_per_step": 1000.0 * float(t[0]) / steps, "units_per_gpu": side_c, "d": 64, "steps": steps,
+            "what": ("in-GPU all-gather + cross-GPU mailbox exchange" if world > 1 else "in-GPU all-gather only")}
+
+
 def c4_leg(som, torch, args, local, rank, world):
     """c4 (BASELINE.json configs[3]: 100x100 hex map, 20,000 terms) online
     training, the first --c4-steps steps.  At N > 1 the map is neuron-sharded
@@ -359,7 +409,9 @@ def c4_leg(som, torch, args, local, rank, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, consistent = float(t[0]), bool(float(t[1]) == -float(t[2]))
-    return {"workload": f"c4: 100x100 hex, 20,000 terms, {n} docs replicated, steps [0, {steps}) of 2 epochs, "
+    probe = exchange_probe(som, torch, args, local, rank, world)
+    return {"exchange_probe": probe,
+            "workload": f"c4: 100x100 hex, 20,000 terms, {n} docs replicated, steps [0, {steps}) of 2 epochs, "
                         f"{'neuron-sharded over ' + str(world) + ' GPUs (in-kernel NVLink winner exchange)' if world > 1 else 'one GPU'}",
             "samples_per_s": steps / (ms_max / 1000.0), "us_per_step": 1000.0 * ms_max / steps,
             "units_per_gpu": (rows * cols + world - 1) // world, "grid": g, "kernel": k,
