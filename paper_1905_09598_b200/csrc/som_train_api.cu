@@ -1,0 +1,325 @@
+// som_train_api.cu — host runtime of libsom, part 2: online training
+// (som_train_online / _csr): argument checks, kernel choice and launch
+// geometry, L2 residency, launch and error reporting.
+
+#include "som_host.h"
+
+using namespace som;
+using namespace som::host;
+
+namespace {
+
+// shared argument checks of som_train_online / som_train_online_csr; on OK
+// *sd holds the schedule and [*t_begin, *t_end) the (resolved) step range
+som_status check_train(som_ctx* h, int64_t n, int32_t epochs, double alpha0, double sigma0, const som_schedule* s,
+                       som_schedule* sd, int64_t* t_begin, int64_t* t_end) {
+    som_schedule_default(sd);
+    if (s) *sd = *s;
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0: no data to train on");
+    if (epochs < 0) return fail(SOM_EINVAL, "epochs must be >= 0");
+    if (!(alpha0 >= 0.0 && alpha0 <= 1.0)) return fail(SOM_EINVAL, "alpha0 must be in [0, 1]");
+    if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
+    if (sd->kind < 0 || sd->kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
+    if (!(sd->k > 0.0) || !std::isfinite(sd->k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
+    if (!(sd->sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
+    if (!(sd->cutoff >= 0.0 && sd->cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
+    const int64_t T = (int64_t)epochs * n;
+    if (*t_end == -1) *t_end = T;
+    if (*t_begin < 0 || *t_end < *t_begin || *t_end > T)
+        return fail(SOM_EINVAL, "bad t-range [%lld, %lld) for T = %lld", (long long)*t_begin, (long long)*t_end,
+                    (long long)T);
+    h->last_ms = 0; h->last_units = 0; h->last_launches = 0;
+    return SOM_OK;
+}
+
+// Unit dealing for the CSR training kernels.  With cyclic dealing (b + s*G)
+// the units of one CTA lie on a few long lattice lines, so the disk of units
+// a pending update touches gives some CTAs many rows and others none, and the
+// step waits for the fullest CTA.  Here unit (i, j) goes to class
+// (alpha*i + j) mod G with alpha chosen so that every class is a near-square
+// sub-lattice (its shortest vector is maximal), then to the first class with
+// room (capacity ceil(NL/G), linear probing): any disk then holds about the
+// same number of rows of every CTA, and the all-dense step keeps its balance.
+void build_unit_tab(int rows, int cols, int topo, int rank, int world, int NL, int G, std::vector<int>& out) {
+    const int S = (NL + G - 1) / G;
+    int best_alpha = cols % G;
+    double best_len = -1.0;
+    for (int al = 1; al < G; ++al) {
+        double mn = 1e300;
+        for (int di = 0; di < rows && di <= 64; ++di) {
+            const int dj0 = (int)((((long long)-al * di) % G + G) % G);
+            for (int dj : {dj0, dj0 - G}) {
+                if (di == 0 && dj == 0) continue;
+                if (dj >= cols || -dj >= cols) continue;   // no such pair of units
+                const double len = topo == 0 ? (double)di * di + (double)dj * dj
+                                             : (double)dj * dj + 0.75 * (double)di * di;
+                mn = std::min(mn, len);
+            }
+        }
+        if (mn > best_len) { best_len = mn; best_alpha = al; }
+    }
+    out.assign((size_t)G * S + G, -1);
+    int* cnt = out.data() + (size_t)G * S;
+    for (int b = 0; b < G; ++b) cnt[b] = 0;
+    for (int l = 0; l < NL; ++l) {
+        const long long u = (long long)rank + (long long)world * l;
+        const long long i = u / cols, j = u % cols;
+        int k = (int)(((long long)best_alpha * i + j) % G);
+        while (cnt[k] >= S) k = (k + 1) % G;
+        out[(size_t)k * S + cnt[k]++] = l;
+    }
+}
+
+som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, int32_t epochs, double alpha0,
+                      double sigma0, const som_schedule& sd, uint64_t seed, int64_t t_begin, int64_t t_end,
+                      int32_t* bmu_log) {
+    const int64_t T = (int64_t)epochs * n;
+    invalidate_w_caches(h);
+    som_status st = SOM_OK;
+    if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
+
+    TrainArgs a{};
+    a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
+    a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->NL;
+    a.rank = h->rank; a.world = h->world;
+    for (int p = 0; p < kMaxRanks; ++p) a.mail[p] = h->peer_mail[p];
+    if (h->world > 1) {
+        for (int p = 0; p < h->world; ++p)
+            if (!h->peer_mail[p]) return fail(SOM_ESTATE, "neuron sharding: peer mailboxes not set (som_comm_set_peers_*)");
+    }
+    a.x_vec4 = (h->dim % 4 == 0) && (csr || (uintptr_t)Xd % 16 == 0);   // densified CSR is aligned
+    // launch geometry.  Register-resident kernel when a CTA's share of W fits
+    // the register file: G minimises (all-gather latency + fp64 distance
+    // time), both measured on B200 (profiles/probe_*_r01.json).  Otherwise
+    // one persistent CTA per SM with W in shared or global memory.
+    // short prototypes (d <= 128): the lane-group kernel (train_small.cu).
+    // G minimises (all-gather latency + per-CTA rounds of work), with the
+    // L2 traffic of the streamed variant when the map exceeds 4 rounds.
+    bool use_small = false;
+    if ((h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_SHORT_ROWS) && a.x_vec4 &&
+        train_small_supported(h->dim)) {
+        auto xchg_us = [](int G) { return G <= 32 ? 0.65 : G <= 64 ? 0.70 : G <= 128 ? 0.85 : 1.65; };
+        const int gmax = std::min(h->NL, h->sm_count);
+        double best = 1e30;
+        int bestG = 0;
+        for (int G : {8, 16, 32, 64, 128, gmax}) {
+            if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
+            if (G < 1 || G > gmax) continue;
+            const int R = small_rounds((h->NL + G - 1) / G, h->dim);
+            double est = xchg_us(G) + 0.35 * R;   // ~0.35 us per round (tools/sweep_small.py, d = 64)
+            // streamed: read + ~60 % written per step at ~12 TB/s of L2 over 148 SMs, pro rata G
+            if (R > 4) est += 2.6 * 4.0 * (double)h->NL * h->dim / (12.0e6 * G / 148.0);
+            if (est < best) { best = est; bestG = G; }
+        }
+        use_small = bestG > 0;
+        a.G = bestG;
+    }
+    if (h->train_mode == SOM_TRAIN_SHORT_ROWS && !use_small)
+        return fail(SOM_EUNSUPPORTED, "short-row kernel needs d <= 128 and d %% 4 == 0");
+    bool use_reg = false;
+    if (!use_small && (h->train_mode == SOM_TRAIN_AUTO || h->train_mode == SOM_TRAIN_W_REGISTERS) && a.x_vec4) {
+        // all-gather latency by grid size (profiles/probe_xchg_r01.json) and
+        // per-CTA F2F-bound distance time: (S + 1) * d conversions at 16/clk
+        // (power-of-two grids measured fastest: 16-64 ~0.6-0.7 us, 128 ~0.8 us,
+        // 48/96/100/112/134/148 all slower; tools/sweep_grid.py on c2)
+        auto xchg_us = [](int G) { return G <= 32 ? 0.65 : G <= 64 ? 0.70 : G <= 128 ? 0.85 : 1.65; };
+        double best = 1e30;
+        int bestG = 0;
+        const int gmax = std::min(h->NL, h->sm_count);
+        std::vector<int> cands = {16, 32, 64, 128};
+        if (gmax <= 32) cands.push_back(gmax);
+        for (int G : cands) {
+            if (h->train_grid > 0) G = std::min(h->train_grid, gmax);
+            if (G < 1 || G > gmax) continue;
+            const int S = (h->NL + G - 1) / G;
+            if (!train_reg_supported(S, h->dim)) continue;
+            const double est = xchg_us(G) + (double)(S + 1) * h->dim / (16.0 * 1965.0);
+            if (est < best) { best = est; bestG = G; }
+        }
+        if (bestG > 0) { use_reg = true; a.G = bestG; }
+    }
+    if (h->train_mode == SOM_TRAIN_W_REGISTERS && !use_reg)
+        return fail(SOM_EUNSUPPORTED, "map share per CTA does not fit registers (or d %% 4 != 0)");
+    if (!use_reg && !use_small) {
+        a.G = std::min(h->NL, h->sm_count);
+        if (h->train_grid > 0) a.G = std::min(a.G, h->train_grid);
+    }
+    a.S = (h->NL + a.G - 1) / a.G;
+    a.t0 = t_begin; a.t1 = t_end; a.seed = seed;
+    a.f_tab = (const double*)h->ftab.p;
+    a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
+    a.cutoff_on = sd.cutoff > 0.0;
+    a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
+    a.trace = h->trace;
+    a.trace_steps = h->trace ? h->trace_steps : 0;
+    a.trace_clk = 0;
+    if (const char* e = std::getenv("SOM_TRACE_CLOCK")) a.trace_clk = std::atoi(e) != 0;
+    size_t smem = train_smem_bytes(a.S, a.dimp, 1);
+    a.w_smem = smem <= (size_t)h->max_smem_optin;
+    if (h->train_mode == SOM_TRAIN_W_SHARED && !a.w_smem)
+        return fail(SOM_EUNSUPPORTED, "W slice (%zu B/CTA) does not fit shared memory", smem);
+    if (h->train_mode == SOM_TRAIN_W_GLOBAL) a.w_smem = 0;
+    if (!a.w_smem) smem = train_smem_bytes(a.S, a.dimp, 0);
+    // maps that do not fit on chip stream from global memory with the
+    // pipelined kernel (train_glb.cu) when its layout applies
+    const bool use_glb = !use_small && !use_reg && !a.w_smem && a.x_vec4 && train_glb_supported(a.S, h->dim);
+    if (use_reg) smem = sizeof(float) * (3 * (size_t)a.dimp + (size_t)a.rows * (a.topo == 0 ? a.cols : 2 * a.cols));
+    if (use_glb) smem = sizeof(float) * 2 * (size_t)a.dimp;
+    if (use_small) {
+        a.w_smem = 0;
+        smem = sizeof(float) * 3 * (size_t)a.dimp +
+               sizeof(double) * ((size_t)a.dimp + a.rows + (a.topo == 0 ? a.cols : 2 * a.cols));
+    }
+    // CSR input: the sparse-distance kernel where W streams from global
+    // memory; on-chip maps (latency-bound, no gain) and layouts it does not
+    // cover train on the densified rows
+    bool use_csr = false;
+    if (csr) {
+        use_csr = !use_small && !use_reg && !a.w_smem && train_csr_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin);
+        if (use_csr) {
+            a.rowptr = csr->rowptr; a.col = csr->col; a.val = csr->val;
+            a.nz_cap = csr_nz_cap(csr->maxnnz);
+            // upper bound of the lattice g2 between any two units (exact for
+            // rect; hex bound takes the half-column offset at the full row span)
+            const double dr = h->rows - 1, dc = h->cols - 1;
+            a.g2max = h->topo == 0 ? dr * dr + dc * dc : 0.25 * (2 * dc + 1) * (2 * dc + 1) + 0.75 * dr * dr;
+            if (h->utab_G != a.G || h->utab_NL != h->NL || h->utab_rank != h->rank || h->utab_world != h->world) {
+                std::vector<int> tab;
+                build_unit_tab(h->rows, h->cols, h->topo, h->rank, h->world, h->NL, a.G, tab);
+                CK(h->utab.ensure(sizeof(int) * tab.size(), h->stream));
+                CK(cudaMemcpyAsync(h->utab.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+                h->utab_G = a.G; h->utab_NL = h->NL; h->utab_rank = h->rank; h->utab_world = h->world;
+            }
+            a.utab = (const int*)h->utab.p;
+            a.ucnt = a.utab + (size_t)a.G * a.S;
+            smem = sizeof(float) * 2 * (size_t)a.dimp + 24 * (size_t)a.nz_cap;
+        } else {
+            CK(h->dense.ensure(sizeof(float) * (size_t)n * h->dim, h->stream));
+            CK(launch_densify(csr->rowptr, csr->col, csr->val, 0, n, h->dim, (float*)h->dense.p, h->stream));
+            a.X = (const float*)h->dense.p;
+        }
+    }
+    if (smem > (size_t)h->max_smem_optin)
+        return fail(SOM_EUNSUPPORTED, "dim %d too large for the x staging ring (%zu B smem)", h->dim, smem);
+
+    // exchange slots: two parities of G slots, each parity on its own 256-byte
+    // lines (a line shared by step t's and step t+1's slots would be written
+    // by fast CTAs while slow ones still poll it)
+    a.xstride = (a.G + 31) & ~31;
+    a.poll_ns = 0;
+    if (const char* e = std::getenv("SOM_POLL_NS")) a.poll_ns = std::max(0, std::atoi(e));
+    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
+    a.xchg = (unsigned long long*)h->xchg.p;
+    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.xstride);
+    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
+
+    const int64_t steps = t_end - t_begin;
+    bool log_dev = bmu_log && is_device_ptr(bmu_log);
+    if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps, h->stream));
+    a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
+
+    // W streamed from global memory every step: keep it resident in L2 with a
+    // persisting access-policy window (random X rows stream past it), undone
+    // after the launch so the caller's stream is left as it was.
+    bool l2_window = false;
+    const char* nowin = std::getenv("SOM_NO_L2_WINDOW");
+    if (!(nowin && std::atoi(nowin)) && !use_reg && !a.w_smem && (!use_small || small_rounds(a.S, h->dim) > 4)) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+        const size_t wbytes = sizeof(float) * (size_t)h->NL * h->dim;
+        int l2_bytes = 0;
+        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, h->device);
+        // only for maps that fit the L2: for a map several times the L2 (c4 on
+        // one GPU, 800 MB) the persisting lines of the window crowd out the
+        // streamed rest of W and the row writes (measured 664 -> 263 us/step
+        // without it)
+        if (max_persist > 0 && max_window > 0 && wbytes <= (size_t)l2_bytes) {
+            const size_t win = std::min(wbytes, (size_t)max_window);
+            const size_t keep = std::min(win, (size_t)max_persist);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep) == cudaSuccess) {
+                cudaStreamAttrValue at{};
+                at.accessPolicyWindow.base_ptr = h->W;
+                at.accessPolicyWindow.num_bytes = win;
+                at.accessPolicyWindow.hitRatio = (float)((double)keep / (double)win);
+                at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                l2_window = cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at) == cudaSuccess;
+            }
+            cudaGetLastError();
+        }
+    }
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if (use_small) CK(launch_train_small(a, h->stream));
+    else if (use_reg) CK(launch_train_reg(a, h->stream));
+    else if (use_csr) CK(launch_train_csr(a, h->stream));
+    else if (use_glb) CK(launch_train_glb(a, h->stream));
+    else CK(launch_train(a, smem, h->stream));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if (l2_window) {   // later launches on the caller's stream get no window
+        cudaStreamAttrValue at{};
+        at.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at);
+        cudaGetLastError();
+    }
+    h->last_grid = a.G;
+    h->last_kernel = use_small ? 5 : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    if (bmu_log && !log_dev)
+        CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (l2_window) {   // the kernel is done: demote its persisting lines and release the set-aside L2
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+    }
+    unsigned abort_flag = 0;
+    CK(cudaMemcpyAsync(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (abort_flag) {
+        h->poisoned = true;
+        return fail(SOM_ECUDA, "training exchange timed out (a CTA or rank stopped publishing its BMU candidate)");
+    }
+    // neuron sharding: clear the own mailbox so the next call's tags cannot
+    // match stale entries (callers barrier between sharded calls)
+    if (h->world > 1) {
+        CK(cudaMemsetAsync(h->mail, 0, sizeof(unsigned long long) * 2 * (size_t)h->world, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms; h->last_units = steps; h->last_launches = 1;
+    return SOM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+som_status som_train_online(som_ctx* h, const float* X, int64_t n, int32_t epochs, double alpha0, double sigma0,
+                            const som_schedule* s, uint64_t seed, int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
+    CHECK_HANDLE(h);
+    if (!X) return fail(SOM_EINVAL, "null X");
+    som_schedule sd;
+    som_status st = check_train(h, n, epochs, alpha0, sigma0, s, &sd, &t_begin, &t_end);
+    if (st) return st;
+    if (t_end == t_begin) return SOM_OK;   // epochs = 0 or empty range: weights unchanged
+    const void* Xd = nullptr;
+    if ((st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd))) return st;
+    return train_impl(h, Xd, nullptr, n, epochs, alpha0, sigma0, sd, seed, t_begin, t_end, bmu_log);
+}
+
+som_status som_train_online_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                                int32_t epochs, double alpha0, double sigma0, const som_schedule* s, uint64_t seed,
+                                int64_t t_begin, int64_t t_end, int32_t* bmu_log) {
+    CHECK_HANDLE(h);
+    som_schedule sd;
+    som_status st = check_train(h, n, epochs, alpha0, sigma0, s, &sd, &t_begin, &t_end);
+    if (st) return st;
+    CsrIn csr{};
+    if ((st = stage_csr(h, rowptr, col, val, n, &csr))) return st;
+    if (t_end == t_begin) return SOM_OK;
+    return train_impl(h, nullptr, &csr, n, epochs, alpha0, sigma0, sd, seed, t_begin, t_end, bmu_log);
+}
+
+}  // extern "C"
