@@ -217,7 +217,7 @@ def mapping_leg(som, torch, args, local, seed, world=1, rank=0):
     cpu = None
     if not args.no_baseline and rank == 0:
         import oracle
-        ns = min(n, 10000)
+        ns = min(n, 40000)                                   # ~10 s on 16 host cores
         t0 = time.perf_counter()
         oracle.map_docs_csr(W, C.indptr[:ns + 1], C.indices[:C.indptr[ns]], C.data[:C.indptr[ns]])
         dt = time.perf_counter() - t0
@@ -681,7 +681,7 @@ def run_b200(args, rank, world, local):
         from synth import init_rows
         Xn = X_host.numpy()
         W0 = init_rows(Xn, N, seed + 1000)
-        steps_s = {"c1": 2000, "c2": 2000, "c3": 20}[args.config]
+        steps_s = {"c1": 20000, "c2": 50000, "c3": 200}[args.config]   # ~10 s of host work (c2)
         r, dt, nt = oracle_train_rate(cfg, Xn, W0, seed, steps_s)
         cpu = {"value": r, "unit": "samples/s", "cores": nt, "kind": "oracle",
                "sample": f"first {steps_s} of {T} training steps of {args.config} ({dt:.1f} s, fp64 oracle, "
