@@ -89,8 +89,9 @@ typedef enum {
     SOM_MAP_AUTO = 0,      /* fastest path available on the device          */
     SOM_MAP_EXACT_F64 = 1, /* fp64-accumulated direct distances (= oracle)   */
     SOM_MAP_3XTF32 = 2,    /* tcgen05 3xTF32 GEMM |x|^2 - 2 x.w + |w|^2 (R20) */
-    SOM_MAP_SPARSE_F64 = 3 /* CSR rows: fp64 sparse identity over the
-                              non-zeros of x (R25); dense rows: as EXACT_F64 */
+    SOM_MAP_SPARSE_F64 = 3 /* fp64 sparse identity over the non-zeros of x
+                              (R25); dense rows are first put in CSR form on
+                              the device */
 } som_map_precision;
 
 /* Fill *s with the defaults above. */

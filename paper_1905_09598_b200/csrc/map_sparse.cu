@@ -29,6 +29,7 @@
 // top-2, warp butterfly top-2; lane 0 writes the tile's two keys, and the
 // exact path's merge kernel combines tiles.
 #include <algorithm>
+#include <cub/device/device_scan.cuh>
 #include <cstdlib>
 
 #include "som_device.cuh"
@@ -241,6 +242,67 @@ __global__ void __launch_bounds__(SP_THREADS, 1) map_sparse_kernel(const SparseA
 }
 
 }  // namespace
+
+// ---------------------------------------------------- dense rows -> CSR
+// (SOM_MAP_SPARSE_F64 on dense input): one warp per row counts and then
+// writes its non-zeros in column order (ballot + popc), so the sparse path
+// sees exactly the CSR form of the rows.
+namespace {
+__global__ void dense_count_kernel(const float* X, int64_t m, int d, int64_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < m;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int c = 0;
+        for (int k = lane; k < d; k += 32) c += X[i * d + k] != 0.0f;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) cnt[i] = c;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[m] = 0;
+}
+
+__global__ void dense_fill_kernel(const float* X, int64_t m, int d, const int64_t* rowptr, int32_t* col, float* val) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < m;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t o = rowptr[i];
+        for (int k0 = 0; k0 < d; k0 += 32) {
+            const int k = k0 + lane;
+            const float v = k < d ? X[i * d + k] : 0.0f;
+            const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0f);
+            if (v != 0.0f) {
+                const int64_t p = o + __popc(mask & ((1u << lane) - 1u));
+                col[p] = k;
+                val[p] = v;
+            }
+            o += __popc(mask);
+        }
+    }
+}
+}  // namespace
+
+size_t dense_csr_temp_bytes(int64_t m) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(m + 1));
+    return b + 256;
+}
+
+// rowptr (m+1) of the CSR form of m dense rows; col/val filled by launch_dense_fill
+cudaError_t launch_dense_rowptr(const float* X, int64_t m, int d, int64_t* cnt, int64_t* rowptr, void* temp,
+                                size_t temp_bytes, cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>((32 * m + 255) / 256, 148 * 16);
+    dense_count_kernel<<<std::max(blocks, 1), 256, 0, st>>>(X, m, d, cnt);
+    size_t tb = temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, cnt, rowptr, (int)(m + 1), st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_fill(const float* X, int64_t m, int d, const int64_t* rowptr, int32_t* col, float* val,
+                              cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>((32 * m + 255) / 256, 148 * 16);
+    dense_fill_kernel<<<std::max(blocks, 1), 256, 0, st>>>(X, m, d, rowptr, col, val);
+    return cudaGetLastError();
+}
 
 int sparse_tile_units(int J) { return 64 * J; }
 int sparse_padded_units(int N, int J) { return (N + 64 * J - 1) / (64 * J) * (64 * J); }

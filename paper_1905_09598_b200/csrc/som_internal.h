@@ -279,6 +279,14 @@ cudaError_t launch_pca_extract(const double* Q, int d, double* v1, double* v2, c
 cudaError_t launch_init_linear(float* W, int rows, int cols, int d, const double* mu, const double* v1,
                                const double* v2, double pc1, double pc2, cudaStream_t st);
 
+// dense rows -> CSR (column order), for SOM_MAP_SPARSE_F64 on dense input:
+// rowptr from per-row counts (cnt: m + 1 int64 scratch), then col / val
+size_t dense_csr_temp_bytes(int64_t m);
+cudaError_t launch_dense_rowptr(const float* X, int64_t m, int d, int64_t* cnt, int64_t* rowptr, void* temp,
+                                size_t temp_bytes, cudaStream_t st);
+cudaError_t launch_dense_fill(const float* X, int64_t m, int d, const int64_t* rowptr, int32_t* col, float* val,
+                              cudaStream_t st);
+
 // CSR -> dense chunk (zero-filled) for the dense mapping paths.
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);

@@ -132,6 +132,36 @@ som_status map_exact_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, in
 
 // Map n rows of the device matrix Xd into device outputs (all device).
 som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches) {
+    if (h->map_precision == SOM_MAP_SPARSE_F64) {
+        // dense rows through the sparse identity (R25): CSR form per chunk of
+        // rows (<= 256 MB of dense input), then the sparse path
+        const int d = h->dim;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, ((int64_t)256 << 20) / (4 * (int64_t)d)));
+        const size_t tb = dense_csr_temp_bytes(chunk);
+        const size_t ints = 2 * ((size_t)chunk + 1);                      // cnt | rowptr (int64)
+        const size_t ent = (size_t)chunk * d;                              // worst case: every entry non-zero
+        CK(h->dense.ensure(sizeof(int64_t) * ints + (sizeof(int32_t) + sizeof(float)) * ent + tb + 512, h->stream));
+        char* base = (char*)h->dense.p;
+        int64_t* cnt = (int64_t*)base;
+        int64_t* rp = cnt + chunk + 1;
+        int32_t* col = (int32_t*)(rp + chunk + 1);
+        float* val = (float*)(col + ent);
+        void* temp = (void*)(((uintptr_t)(val + ent) + 255) & ~(uintptr_t)255);
+        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+            const int64_t m = std::min(chunk, n - r0);
+            const float* Xc = Xd + r0 * d;
+            CK(launch_dense_rowptr(Xc, m, d, cnt, rp, temp, tb, h->stream));
+            CK(launch_dense_fill(Xc, m, d, rp, col, val, h->stream));
+            *launches += 3;
+            int64_t nnz = 0;
+            CK(cudaMemcpyAsync(&nnz, rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            CsrIn c{rp, col, val, 0, nnz};
+            som_status st = map_csr_dev(h, c, m, b1 + r0, b2 ? b2 + r0 : nullptr, d2 ? d2 + r0 : nullptr, launches);
+            if (st) return st;
+        }
+        return SOM_OK;
+    }
     if (use_tc(h, n)) {
         auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
             return launch_split_rows(Xd + r0 * h->dim, m, h->dim, hi, lo, nrm, h->stream);

@@ -197,3 +197,24 @@ def test_integer_widening_is_exact(som, monkeypatch, cfg):
         assert np.array_equal(a, b)
     ob1, ob2, od1, m12, m23 = oracle.map_docs(W, X, want_margins=True)
     _check(*outs[0], ob1, ob2, od1, m12, m23)
+
+
+def test_dense_rows_through_sparse_path(som):
+    """SOM_MAP_SPARSE_F64 on dense rows: the rows are put in CSR form on the
+    device (column order), so every output equals the CSR-input call bit for
+    bit; QE/TE through som_errors likewise."""
+    C = bank_corpus(4000, 3000, seed=81)
+    X = C.dense()
+    W = _codebook(X, 400, 82)
+    with som.SOM(20, 20, 3000, 1) as m:
+        m.set_weights(W)
+        som.som_set_map_precision(m.h, som.SOM_MAP_SPARSE_F64)
+        a = m.map(X)
+        qa, ta = m.errors(X)
+        b = m.map_csr(C.indptr, C.indices, C.data, C.n)
+        qb, tb = m.errors_csr(C.indptr, C.indices, C.data, C.n)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    assert qa == qb and ta == tb
+    ob1, ob2, od1, m12, m23 = oracle.map_docs(W, X, want_margins=True)
+    _check(*a, ob1, ob2, od1, m12, m23)
