@@ -571,6 +571,9 @@ def run_b200(args, rank, world, local):
     stream = torch.cuda.current_stream()
     m = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
     som.som_set_stream(m.h, stream)
+    # mapping / QE / TE of the step through the exact sparse identity (R25):
+    # the TF-IDF rows are put in CSR form on the device
+    som.som_set_map_precision(m.h, som.SOM_MAP_SPARSE_F64)
     b1 = torch.empty(n, dtype=torch.int32, device="cuda")
     b2 = torch.empty(n, dtype=torch.int32, device="cuda")
     d1 = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -696,7 +699,8 @@ def run_b200(args, rank, world, local):
         "config": {"workload": args.config, "map": f"{cfg['rows']}x{cfg['cols']} {'hex' if cfg['topo'] else 'rect'}",
                    "docs": n, "terms": d, "epochs": cfg["epochs"], "samples_per_step": T,
                    "alpha0": ALPHA0, "sigma0": cfg["sigma0"], "cutoff": 1e-4, "parallelism": f"replicas{world}",
-                   "l2": "flushed between timed steps (256 MB write)"},
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "mapping": "exact sparse identity (SOM_MAP_SPARSE_F64, R25)"},
         "secondary": {"map_docs_per_s": n / (ph_mean["map_ms"] / 1000.0),
                       "train_samples_per_s_kernel": T / (train_ms / 1000.0),
                       "us_per_training_step": 1000.0 * train_ms / T, "phase_ms": ph_mean,
