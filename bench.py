@@ -192,6 +192,22 @@ def mapping_leg(som, torch, args, local, seed, world=1, rank=0):
 
     ms, launches = timed(som.SOM_MAP_AUTO)
     sp_b1 = b1.cpu().numpy()
+    # end to end through the C ABI with pinned HOST buffers: the CSR arrays
+    # go host -> device and bmu1, bmu2, D1 come back inside the timed call
+    hrp, hci, hva = (torch.from_numpy(a).pin_memory() for a in (C.indptr, C.indices, C.data))
+    hb1 = torch.empty(n, dtype=torch.int32).pin_memory()
+    hb2 = torch.empty(n, dtype=torch.int32).pin_memory()
+    hd1 = torch.empty(n, dtype=torch.float32).pin_memory()
+    som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)     # warm-up (staging buffers)
+    e2e = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)
+        e2e.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e)
+    h2d_map = hrp.numel() * 8 + hci.numel() * 4 + hva.numel() * 4
+    d2h_map = n * 12
     # document sharding: every rank maps its own n documents;
     # the job time is the slowest rank's, the error sums are all-reduced
     qe_l, te_l = som.som_errors_csr(mm.h, rp, ci, va, n)
@@ -227,6 +243,8 @@ def mapping_leg(som, torch, args, local, seed, world=1, rank=0):
     return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms "
                         f"per GPU, document-sharded over {world} GPU(s)",
             "docs_per_s": world * n / (ms_max / 1000.0), "ms": ms_max, "launches": launches, "n_gpus": world,
+            "e2e": {"docs_per_s_rank0": n / e2e_s, "h2d_bytes": h2d_map, "d2h_bytes": d2h_map,
+                    "what": "som_map_csr with pinned host CSR arrays and host outputs, wall clock per call"},
             "scaling": "weak", "qe": qe, "te": te, "errors_ms_rank0": err_ms,
             "path": "exact fp64 sparse identity (SOM_MAP_SPARSE_F64, AUTO)",
             "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T, integer widening> (rank 0)",
