@@ -169,8 +169,17 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * kernel 0 = W in global memory (generic), 1 = W in shared memory,
  * 2 = W in registers, 3 = W in global memory (pipelined, d % 4 == 0),
  * 4 = W in global memory with the sparse distance path (CSR input),
- * 5 = short-row kernel (SOM_TRAIN_SHORT_ROWS). */
+ * 5 = short-row kernel (SOM_TRAIN_SHORT_ROWS),
+ * 6 = W in registers with the winner exchange of step t overlapped with the
+ *     distance pass of step t+1 (train_spec.cu, R32; same results
+ *     as kernel 2; opt-in with the environment variable SOM_TRAIN_SPEC=1
+ *     where kernel 2 applies on one GPU, measured slower at c1/c2). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
+
+/* Kernel 6 only: number of steps of the last som_train_online call whose
+ * speculative winner could not be certified (near-tie) and that took the
+ * exact fallback pass (0 for other kernels).  *count >= 0. */
+som_status som_last_spec_fallbacks(som_ctx *h, int64_t *count);
 
 /* ---- Neuron sharding: online training of one map across
  * `world` GPUs (one process or handle per rank).  Rank r holds the units

@@ -74,6 +74,7 @@ struct som_ctx {
     int train_mode = SOM_TRAIN_AUTO;
     int train_grid = 0;       // 0 = auto
     int last_grid = 0, last_kernel = -1;
+    int64_t last_spec_fallbacks = 0;
     unsigned long long* trace = nullptr;   // caller-owned device buffer (som_set_trace)
     int trace_steps = 0;
     // scratch

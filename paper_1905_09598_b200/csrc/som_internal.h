@@ -56,6 +56,8 @@ struct TrainArgs {
     // utab[b * S + s], s < ucnt[b]; NULL = cyclic (b + s * G)
     const int* utab;
     const int* ucnt;
+    // train_spec.cu: count of steps that took the exact fallback (nullable)
+    unsigned long long* spec_fallbacks;
 };
 
 constexpr int kTracePhases = 8;
@@ -168,6 +170,8 @@ cudaError_t launch_train(const TrainArgs& a, size_t smem, cudaStream_t st);
 // per-CTA share of W (S units x ceil(d/2048) float4 chunks per thread).
 bool train_reg_supported(int S, int dim);
 cudaError_t launch_train_reg(const TrainArgs& a, cudaStream_t st);
+bool train_spec_supported(int S, int dim, int G, int world);
+cudaError_t launch_train_spec(const TrainArgs& a, cudaStream_t st);
 // pipelined global-memory variant (train_glb.cu) for maps that do not fit on chip
 bool train_glb_supported(int S, int dim);
 cudaError_t launch_train_glb(const TrainArgs& a, cudaStream_t st);

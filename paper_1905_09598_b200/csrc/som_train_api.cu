@@ -209,10 +209,20 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     a.xstride = (a.G + 31) & ~31;
     a.poll_ns = 0;
     if (const char* e = std::getenv("SOM_POLL_NS")) a.poll_ns = std::max(0, std::atoi(e));
-    CK(h->xchg.ensure(sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
+    // (kernel 6: a second word per CTA, [2][2][xstride]); then the abort flag
+    // and the fallback counter
+    const size_t xwords = 4 * (size_t)a.xstride;
+    CK(h->xchg.ensure(sizeof(unsigned long long) * xwords + 64, h->stream));
     a.xchg = (unsigned long long*)h->xchg.p;
-    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * 2 * (size_t)a.xstride);
-    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * 2 * (size_t)a.xstride + 64, h->stream));
+    a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords);
+    a.spec_fallbacks = (unsigned long long*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords + 8);
+    CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords + 64, h->stream));
+    bool use_spec = false;
+    if (use_reg && train_spec_supported(a.S, h->dim, a.G, h->world)) {
+        // measured slower than kernel 2 on c1/c2 (R32): opt-in
+        const char* e = std::getenv("SOM_TRAIN_SPEC");
+        use_spec = e && std::atoi(e) != 0;
+    }
 
     const int64_t steps = t_end - t_begin;
     bool log_dev = bmu_log && is_device_ptr(bmu_log);
@@ -252,6 +262,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     }
     CK(cudaEventRecord(h->ev0, h->stream));
     if (use_small) CK(launch_train_small(a, h->stream));
+    else if (use_spec) CK(launch_train_spec(a, h->stream));
     else if (use_reg) CK(launch_train_reg(a, h->stream));
     else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
@@ -264,7 +275,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_small ? 5 : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_spec ? 6 : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -276,6 +287,13 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     unsigned abort_flag = 0;
     CK(cudaMemcpyAsync(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    h->last_spec_fallbacks = 0;
+    if (use_spec) {
+        unsigned long long fb = 0;
+        CK(cudaMemcpyAsync(&fb, a.spec_fallbacks, sizeof(fb), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->last_spec_fallbacks = (int64_t)fb;
+    }
     if (abort_flag) {
         h->poisoned = true;
         return fail(SOM_ECUDA, "training exchange timed out (a CTA or rank stopped publishing its BMU candidate)");

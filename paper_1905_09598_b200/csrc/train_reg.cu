@@ -27,41 +27,6 @@ namespace {
 constexpr int NT = kTrainThreads;
 constexpr int NW = kTrainWarps;
 
-__device__ __forceinline__ float4 eq1u(float h, float4 w, float4 x) {
-    // Eq. 1 per element: w + h (x - w) as fmaf(h, RN(x - w), w)  (R11)
-    w.x = fmaf(h, x.x - w.x, w.x);
-    w.y = fmaf(h, x.y - w.y, w.y);
-    w.z = fmaf(h, x.z - w.z, w.z);
-    w.w = fmaf(h, x.w - w.w, w.w);
-    return w;
-}
-
-// Warp sum of SMAX per-lane values with a multi-value butterfly: at each of
-// the first log2(SMAX) levels a lane keeps half of its slots and sends the
-// other half, so the warp issues 2*(SMAX-1) + 2*(5 - log2 SMAX) shuffles
-// instead of 10*SMAX.  Returns the full warp sum of slot `*slot` in lanes
-// whose low (5 - log2 SMAX) bits are zero.
-template <int SMAX>
-__device__ __forceinline__ double butterfly_sum(double (&v)[SMAX], int lane, int* slot) {
-    int sl = 0;
-#pragma unroll
-    for (int width = SMAX, off = 16; width > 1; width >>= 1, off >>= 1) {
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < width / 2; ++i) {
-            const double send = upper ? v[i] : v[i + width / 2];
-            const double keep = upper ? v[i + width / 2] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-        sl = sl * 2 + (upper ? 1 : 0);
-    }
-    double x = v[0];
-#pragma unroll
-    for (int off = 16 / SMAX; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-    *slot = sl;
-    return x;
-}
-
 template <int SMAX, int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a) {
     __shared__ double part[NW][SMAX];        // per-warp partial distance of each unit

@@ -27,11 +27,16 @@ ms, units, _ = som.som_last_stats(m.h)
 G, k = som.som_last_train_config(m.h)
 t = tr.view(148, steps, 8)[:G].cpu().numpy().astype(np.float64)[:, 200:]
 names = ["fused+reduce", "issue_x+barA", "w0 key", "publish+poll", "h compute", "x shift/read", "barB"]
+if k == 6:   # train_spec.cu phases
+    names = ["bounds+publish", "wait+h", "(pass end, thread 32)", "barA+totals", "-", "-", "-"]
 print(f"{sys.argv[1]} t=[{tb},{tb + steps}) G={G} kernel={k}: {1000 * ms / units:.3f} us/step (event)")
 d = np.diff(t, axis=2)                        # [G][steps][7]
 for i in range(7):
     med = np.median(d[:, :, i], axis=1)       # per CTA
     print(f"  {names[i]:14s} median over CTAs {np.median(med):6.0f} ns  min {med.min():6.0f}  max {med.max():6.0f}")
+if k == 6:
+    ps = np.median(t[:, 1:, 3] - t[:, :-1, 4], axis=1)
+    print(f"  pass (totals(t-1) -> thread 32 pass end): median {np.median(ps):.0f}  max {ps.max():.0f}")
 pub = t[:, :, 3]                              # publish time per CTA per step
 spread = pub.max(0) - pub.min(0)
 late = np.argmax(pub, axis=0)
