@@ -113,7 +113,7 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
         }
         if (__all_sync(0xffffffffu, ok)) { gmin = warp_min_u64(m); break; }
         if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
-        if (a.poll_ns) __nanosleep(a.poll_ns);
+        if (a.poll_ns > 0) __nanosleep(a.poll_ns);
     }
     if (a.world <= 1) return gmin;
     const size_t par = (size_t)(t & 1) * a.world;

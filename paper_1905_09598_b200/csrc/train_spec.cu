@@ -75,7 +75,7 @@ __device__ __forceinline__ unsigned long long spec_wait(const TrainArgs& a, uint
         if (__all_sync(0xffffffffu, ok)) break;
         if (spins == 0 && tr) tr[5] = trace_now(a.trace_clk);
         if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
-        if (a.poll_ns) __nanosleep(a.poll_ns);
+        if (a.poll_ns > 0) __nanosleep(a.poll_ns);
     }
     if (tr) { tr[6] = trace_now(a.trace_clk); tr[4] = spins; }
     unsigned long long m = ~0ull;
