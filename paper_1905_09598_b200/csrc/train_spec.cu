@@ -37,6 +37,7 @@ namespace {
 constexpr int NT = kTrainThreads;
 constexpr int NW = kTrainWarps;
 constexpr int kSpecMaxG = 128;            // exchange slots held per lane <= 4
+constexpr int kSpecPass = 32 * (NW - NW / 4);   // pass threads per CTA
 
 __device__ __forceinline__ unsigned long long* spec_slot_a(const TrainArgs& a, uint32_t q) {
     return a.xchg + (size_t)(q & 1) * a.xstride;
@@ -107,7 +108,11 @@ __device__ __forceinline__ unsigned long long spec_wait(const TrainArgs& a, uint
 template <int SMAX, int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a) {
     constexpr int NV = 2 * SMAX;             // per unit: A, P
-    constexpr int NP = NT - 32;              // pass threads (warps 1..15)
+    // pass threads: every warp except those of sub-partition 0 (warps 0, 4,
+    // 8, 12), so that the control warp has its scheduler to itself
+    constexpr int NPW = NW - NW / 4;
+    constexpr int NP = 32 * NPW;
+    static_assert(NP == kSpecPass, "pass thread count");
     __shared__ double part[2][NW][NV + 2];   // per-warp partials of the pass (+ Delta, ||x||^2), by step parity
     __shared__ double partx[NW][SMAX];       // per-warp partials of the exact (fallback) pass
     __shared__ float s_h[2][SMAX];           // h of this CTA's units for the update of step t (parity t)
@@ -118,7 +123,8 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
 
     const int b = blockIdx.x, G = a.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int pt = threadIdx.x - 32;         // pass thread index (< 0: control warp)
+    const int pw = (warp & 3) ? warp - (warp >> 2) - 1 : -1;   // pass warp index (< 0: control / idle)
+    const int pt = pw >= 0 ? pw * 32 + lane : -1;
     const int Sb = (a.N - b + G - 1) / G;
     const int d4 = a.dimp >> 2;
     const float4* W4 = reinterpret_cast<const float4*>(a.W);
@@ -190,9 +196,9 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
         }
         int slot;
         const double r = butterfly_sum<NV>(v, lane, &slot);
-        if ((lane & (32 / NV - 1)) == 0) part[par][warp][slot] = r;
+        if ((lane & (32 / NV - 1)) == 0) part[par][pw][slot] = r;
         const double rx = butterfly_sum<2>(xv, lane, &slot);
-        if ((lane & 15) == 0) part[par][warp][NV + slot] = rx;
+        if ((lane & 15) == 0) part[par][pw][NV + slot] = rx;
     };
     // control warp, lane l: sums of unit l & (SMAX-1): uA = A, uP = P,
     // usA = sqrt(A); the step's Delta, sqrt(Delta), ||x|| (sqrt bounds
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
             double tot = 0.0;
             if (lane < NV + 2) {
 #pragma unroll
-                for (int w8 = 1; w8 < NW; ++w8) tot += part[par][w8][lane];
+                for (int w8 = 0; w8 < NPW; ++w8) tot += part[par][w8][lane];
             }
             const double A = __shfl_sync(0xffffffffu, tot, su);
             const double P = __shfl_sync(0xffffffffu, tot, SMAX + su);
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
                 if (stop) s_abort = 1;
             }
             TRACE(2);
-        } else {
+        } else if (pt >= 0) {
             // ---- pass: update t-1, sums of step t+1 (overlaps the exchange)
 #pragma unroll
             for (int j = 0; j < KJ; ++j) { xm[j] = xc[j]; xc[j] = xn[j]; }
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
                 }
                 int slot;
                 const double r = butterfly_sum<SMAX>(v, lane, &slot);
-                if ((lane & (32 / SMAX - 1)) == 0) partx[warp][slot] = r;
+                if ((lane & (32 / SMAX - 1)) == 0) partx[pw][slot] = r;
             }
             __syncthreads();
             if (warp == 0) {
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
                 if (lane < SMAX && lane < Sb) {
                     double d = 0.0;
 #pragma unroll
-                    for (int w8 = 1; w8 < NW; ++w8) d += partx[w8][lane];
+                    for (int w8 = 0; w8 < NPW; ++w8) d += partx[w8][lane];
                     key = make_key((float)d, uid);
                 }
                 key = warp_min_u64(key);
@@ -441,13 +447,13 @@ int smax_of(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 
 // exchange stays in train_reg.cu), G <= 128.
 bool train_spec_supported(int S, int dim, int G, int world) {
     if (world != 1 || G > kSpecMaxG || dim % 4 != 0) return false;
-    const int kj = ((dim / 4) + NT - 33) / (NT - 32);
+    const int kj = ((dim / 4) + kSpecPass - 1) / kSpecPass;
     const int sm = smax_of(S);
     return kj <= 4 && sm <= 8 && sm * kj <= (kj == 4 ? 4 : 8);
 }
 
 cudaError_t launch_train_spec(const TrainArgs& a, cudaStream_t st) {
-    const int kj = ((a.dimp / 4) + NT - 33) / (NT - 32);
+    const int kj = ((a.dimp / 4) + kSpecPass - 1) / kSpecPass;
     const int sm = smax_of(a.S);
 #define TRY(SM, K) if (sm == SM && kj == K) return launch_one<SM, K>(a, st)
     TRY(1, 1); TRY(2, 1); TRY(4, 1); TRY(8, 1);

@@ -3,7 +3,7 @@ sys.path.insert(0, '/root/repo')
 import numpy as np, torch
 from paper_1905_09598_b200 import som
 from synth import CONFIGS, bank_corpus, init_rows
-cfg = dict(CONFIGS["c2"]); steps = 3000; tb = 250000
+cfg = dict(CONFIGS["c2"]); steps = 3000; tb = int(sys.argv[1]) if len(sys.argv) > 1 else 250000
 C = bank_corpus(cfg["n"], cfg["d"], seed=1)
 X = torch.from_numpy(C.dense()).cuda()
 W0 = torch.from_numpy(init_rows(C.dense(), cfg["rows"] * cfg["cols"], 1001)).cuda()
