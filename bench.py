@@ -707,6 +707,15 @@ def run_b200(args, rank, world, local):
         cpu = {"value": r, "unit": "samples/s", "cores": nt, "kind": "oracle",
                "sample": f"first {steps_s} of {T} training steps of {args.config} ({dt:.1f} s, fp64 oracle, "
                          f"OpenMP over units)"}
+        # the oracle on one core as well (a shorter prefix)
+        steps_1 = max(1, steps_s // 25)
+        oracle.set_num_threads(1)
+        try:
+            r1, dt1, _ = oracle_train_rate(cfg, Xn, W0, seed, steps_1)
+        finally:
+            oracle.set_num_threads(nt)
+        cpu["single_core"] = {"value": r1, "unit": "samples/s", "cores": 1,
+                              "sample": f"first {steps_1} training steps ({dt1:.1f} s)"}
 
     ph_mean = {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
     line = {
