@@ -685,7 +685,8 @@ def run_b200(args, rank, world, local):
 
     g_used, k_used = som.som_last_train_config(m.h)
     kname = {0: "som_train_kernel (W global)", 1: "som_train_kernel (W smem)",
-             2: "som_train_reg_kernel (W registers)"}.get(k_used, "?")
+             2: "som_train_reg_kernel (W registers)", 6: "som_train_spec_kernel (W registers, overlapped exchange)",
+             7: "som_train_spec_kernel then som_train_reg_kernel (W registers; one call, two launches)"}.get(k_used, "?")
     mapping = mapping_leg(som, torch, args, local, seed, world, rank) if args.map_docs > 0 else None
     train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
     table3 = table3_leg(som, torch, args, local, seed) if args.table3_steps > 0 else None

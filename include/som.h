@@ -172,8 +172,12 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * 5 = short-row kernel (SOM_TRAIN_SHORT_ROWS),
  * 6 = W in registers with the winner exchange of step t overlapped with the
  *     distance pass of step t+1 (train_spec.cu, R32; same results
- *     as kernel 2; opt-in with the environment variable SOM_TRAIN_SPEC=1
- *     where kernel 2 applies on one GPU, measured slower at c1/c2). */
+ *     as kernel 2),
+ * 7 = kernel 6 for the steps whose neighbourhood still covers >= 70 % of
+ *     the map, then kernel 2 (two launches in one call): the AUTO choice
+ *     where kernel 2 applies on one GPU with >= 8192 prototype elements per
+ *     CTA and no forced mode or grid.  SOM_TRAIN_SPEC=1 forces kernel 6 for
+ *     the whole range, SOM_TRAIN_SPEC=0 kernel 2. */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* Kernel 6 only: number of steps of the last som_train_online call whose

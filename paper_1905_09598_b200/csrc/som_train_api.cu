@@ -217,11 +217,48 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords);
     a.spec_fallbacks = (unsigned long long*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords + 8);
     CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords + 64, h->stream));
+    // kernel 6 (train_spec.cu, R32): SOM_TRAIN_SPEC=1 for the whole range,
+    // =0 never; AUTO (unset, no forced mode or grid, one GPU): kernel 6 on a
+    // balanced grid for the steps whose neighbourhood still covers >= 70 %
+    // of the map (there it beats kernel 2, whose pass grows with the
+    // updated units), then kernel 2 (tools/spec_windows.py, R32).
+    // Both give identical results and the t-range split is exact.
     bool use_spec = false;
-    if (use_reg && train_spec_supported(a.S, h->dim, a.G, h->world)) {
-        // measured slower than kernel 2 on c1/c2 (R32): opt-in
-        const char* e = std::getenv("SOM_TRAIN_SPEC");
-        use_spec = e && std::atoi(e) != 0;
+    const char* spec_env = std::getenv("SOM_TRAIN_SPEC");
+    if (use_reg && spec_env && std::atoi(spec_env) != 0 && train_spec_supported(a.S, h->dim, a.G, h->world))
+        use_spec = true;
+    int64_t t_split = t_begin;   // hybrid: kernel 6 on [t_begin, t_split), kernel 2 after
+    int G6 = 0;
+    if (use_reg && !spec_env && h->train_mode == SOM_TRAIN_AUTO && h->train_grid == 0 && h->world == 1 &&
+        (int64_t)a.S * h->dim >= 8192) {
+        const int g6 = (h->NL + a.S - 1) / a.S;
+        if (train_spec_supported(a.S, h->dim, g6, 1)) {
+            // units inside the cutoff around the map centre at step t (non-increasing in t)
+            const int ic = h->rows / 2, jc = h->cols / 2;
+            auto covered = [&](int64_t t) {
+                double f;
+                fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
+                double sigma = std::max(sd.sigma_min, sigma0 * f);
+                const double r2 = sd.cutoff > 0.0 ? 2.0 * sigma * sigma * std::log(1.0 / sd.cutoff) : INFINITY;
+                int64_t cnt = 0;
+                for (int i = 0; i < h->rows; ++i)
+                    for (int j = 0; j < h->cols; ++j) {
+                        const double di = i - ic;
+                        double g2;
+                        if (h->topo == 0) { const double dj = j - jc; g2 = di * di + dj * dj; }
+                        else { const double dx = 2.0 * (j - jc) + ((i & 1) - (ic & 1)); g2 = 0.25 * dx * dx + 0.75 * di * di; }
+                        cnt += g2 <= r2;
+                    }
+                return cnt >= (int64_t)std::ceil(0.7 * h->NL);
+            };
+            int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) not covered
+            while (lo < hi) {
+                const int64_t mid = lo + (hi - lo) / 2;
+                if (covered(mid)) lo = mid + 1; else hi = mid;
+            }
+            t_split = lo;
+            if (t_split > t_begin) G6 = g6;
+        }
     }
 
     const int64_t steps = t_end - t_begin;
@@ -261,8 +298,29 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         }
     }
     CK(cudaEventRecord(h->ev0, h->stream));
+    int launches = 1;
     if (use_small) CK(launch_train_small(a, h->stream));
     else if (use_spec) CK(launch_train_spec(a, h->stream));
+    else if (G6 > 0) {
+        TrainArgs a6 = a;
+        a6.G = G6;
+        a6.S = (h->NL + G6 - 1) / G6;
+        a6.xstride = (G6 + 31) & ~31;
+        a6.t1 = t_split;
+        CK(launch_train_spec(a6, h->stream));
+        if (t_split < t_end) {
+            // fresh exchange slots (the abort flag and the fallback counter stay)
+            CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords, h->stream));
+            TrainArgs a2 = a;
+            a2.t0 = t_split;
+            a2.f_tab = a.f_tab + (t_split - t_begin);
+            if (a2.bmu_log) a2.bmu_log = a.bmu_log + (t_split - t_begin);
+            a2.trace = nullptr;
+            a2.trace_steps = 0;
+            CK(launch_train_reg(a2, h->stream));
+            launches = 2;
+        }
+    }
     else if (use_reg) CK(launch_train_reg(a, h->stream));
     else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
@@ -275,7 +333,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_small ? 5 : use_spec ? 6 : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -288,7 +346,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     CK(cudaMemcpyAsync(&abort_flag, a.abort_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->last_spec_fallbacks = 0;
-    if (use_spec) {
+    if (use_spec || G6 > 0) {
         unsigned long long fb = 0;
         CK(cudaMemcpyAsync(&fb, a.spec_fallbacks, sizeof(fb), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -306,7 +364,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-    h->last_ms = ms; h->last_units = steps; h->last_launches = 1;
+    h->last_ms = ms; h->last_units = steps; h->last_launches = launches;
     return SOM_OK;
 }
 
