@@ -174,10 +174,11 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  *     distance pass of step t+1 (train_spec.cu, R32; same results
  *     as kernel 2),
  * 7 = kernel 6 for the steps whose neighbourhood still covers >= 70 % of
- *     the map, then kernel 2 (two launches in one call): the AUTO choice
- *     where kernel 2 applies on one GPU with >= 8192 prototype elements per
- *     CTA and no forced mode or grid.  SOM_TRAIN_SPEC=1 forces kernel 6 for
- *     the whole range, SOM_TRAIN_SPEC=0 kernel 2. */
+ *     the map (SOM_SPEC_COVER), then kernel 2 (two launches in one call).
+ * Where kernel 2 applies on one GPU the environment variable SOM_TRAIN_SPEC
+ * selects: unset or 0 = kernel 2 (default), 1 = kernel 6 for the whole
+ * range, 2 = kernel 7 (needs >= 8192 prototype elements per CTA and no
+ * forced mode or grid).  All give identical results. */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* Kernel 6 only: number of steps of the last som_train_online call whose

@@ -217,24 +217,26 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     a.abort_flag = (unsigned*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords);
     a.spec_fallbacks = (unsigned long long*)((char*)h->xchg.p + sizeof(unsigned long long) * xwords + 8);
     CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords + 64, h->stream));
-    // kernel 6 (train_spec.cu, R32): SOM_TRAIN_SPEC=1 for the whole range,
-    // =0 never; AUTO (unset, no forced mode or grid, one GPU): kernel 6 on a
-    // balanced grid for the steps whose neighbourhood still covers >= 70 %
-    // of the map (there it beats kernel 2, whose pass grows with the
-    // updated units), then kernel 2 (tools/spec_windows.py, R32).
-    // Both give identical results and the t-range split is exact.
+    // kernel 6 (train_spec.cu, R32): SOM_TRAIN_SPEC=1 for the whole range;
+    // =2 (no forced mode or grid, one GPU): kernel 6 on a balanced grid for
+    // the steps whose neighbourhood still covers >= 70 % of the map, then
+    // kernel 2 (tools/spec_windows.py); unset / 0: kernel 2.  Both give
+    // identical results and the t-range split is exact; the speed relative
+    // to kernel 2 varies by box (-4 % .. +3 % at c2), so not the default.
     bool use_spec = false;
     const char* spec_env = std::getenv("SOM_TRAIN_SPEC");
-    if (use_reg && spec_env && std::atoi(spec_env) != 0 && train_spec_supported(a.S, h->dim, a.G, h->world))
-        use_spec = true;
+    const int spec_mode = spec_env ? std::atoi(spec_env) : 0;
+    if (use_reg && spec_mode == 1 && train_spec_supported(a.S, h->dim, a.G, h->world)) use_spec = true;
     int64_t t_split = t_begin;   // hybrid: kernel 6 on [t_begin, t_split), kernel 2 after
     int G6 = 0;
-    if (use_reg && !spec_env && h->train_mode == SOM_TRAIN_AUTO && h->train_grid == 0 && h->world == 1 &&
+    if (use_reg && spec_mode == 2 && h->train_mode == SOM_TRAIN_AUTO && h->train_grid == 0 && h->world == 1 &&
         (int64_t)a.S * h->dim >= 8192) {
         const int g6 = (h->NL + a.S - 1) / a.S;
         if (train_spec_supported(a.S, h->dim, g6, 1)) {
             // units inside the cutoff around the map centre at step t (non-increasing in t)
             const int ic = h->rows / 2, jc = h->cols / 2;
+            double cover = 0.7;   // SOM_SPEC_COVER: coverage threshold of the hand-over
+            if (const char* e = std::getenv("SOM_SPEC_COVER")) cover = std::atof(e);
             auto covered = [&](int64_t t) {
                 double f;
                 fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
@@ -249,7 +251,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
                         else { const double dx = 2.0 * (j - jc) + ((i & 1) - (ic & 1)); g2 = 0.25 * dx * dx + 0.75 * di * di; }
                         cnt += g2 <= r2;
                     }
-                return cnt >= (int64_t)std::ceil(0.7 * h->NL);
+                return cnt >= (int64_t)std::ceil(cover * h->NL);
             };
             int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) not covered
             while (lo < hi) {

@@ -86,3 +86,26 @@ def test_spec_c2_prefix_equals_register_kernel(som, monkeypatch):
     assert np.array_equal(log6, log2)
     assert np.array_equal(W6, W2)
     print(f" [c2 prefix: {fb} of {T} steps took the exact fallback]", end="")
+
+
+def test_hybrid_c2_full_schedule_equals_register_kernel(som, monkeypatch):
+    """SOM_TRAIN_SPEC=2 (kernel id 7): kernel 6 while the neighbourhood covers
+    >= 70 % of the map, then kernel 2, over the full c2 schedule (500,000
+    steps): two launches, and the BMU log and weights of kernel 2 alone
+    (which test_c2_full_schedule checks against the oracle) bit for bit."""
+    cfg = dict(CONFIGS["c2"])
+    C = bank_corpus(cfg["n"], cfg["d"], seed=1)
+    X = C.dense()
+    W0 = init_rows(X, cfg["rows"] * cfg["cols"], 1001)
+    out = {}
+    for mode in ("2", "0"):
+        monkeypatch.setenv("SOM_TRAIN_SPEC", mode)
+        with som.SOM(cfg["rows"], cfg["cols"], cfg["d"], cfg["topo"]) as m:
+            m.set_weights(W0)
+            log = np.full(cfg["n"] * cfg["epochs"], -7, np.int32)
+            m.train_online(X, epochs=cfg["epochs"], alpha0=0.1, sigma0=cfg["sigma0"], seed=1, bmu_log=log)
+            _, _, launches = som.som_last_stats(m.h)
+            out[mode] = (m.get_weights(), log, som.som_last_train_config(m.h)[1], launches)
+    assert out["2"][2:] == (7, 2) and out["0"][2:] == (2, 1)
+    assert np.array_equal(out["2"][1], out["0"][1])
+    assert np.array_equal(out["2"][0], out["0"][0])
