@@ -116,7 +116,9 @@ som_status som_init_random(som_ctx *h, const float *X, int64_t n, uint64_t seed)
 
 /* Online ("standard") SOM training: for each step
  * t in [t_begin, t_end) of T = epochs * n steps (R7):
- *   i_t   = sample index: t-th SplitMix64(seed) output mapped to [0,n) (R8)
+ *   i_t   = sample index: t-th SplitMix64(seed) output mapped to [0,m) (R8)
+ *           over the m non-zero rows (all-zero rows are never drawn, S:104,
+ *           S:218; SOM_EEMPTY when every row is zero)
  *   c_t   = argmin_u (RN_fp32(sum_k (x_k - w_uk)^2 in fp64), u)  (R9, R10)
  *   w_u  <- fmaf(h_u, x - w_u, w_u) for units within the cutoff   (Eq. 1, R11)
  *   h_u   = RN_fp32(alpha_t exp(-g2(u,c_t) / (2 sigma_t^2)))      (R4)
@@ -171,14 +173,17 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * 4 = W in global memory with the sparse distance path (CSR input),
  * 5 = short-row kernel (SOM_TRAIN_SHORT_ROWS),
  * 6 = W in registers with the winner exchange of step t overlapped with the
- *     distance pass of step t+1 (train_spec.cu, R32; same results
- *     as kernel 2),
+ *     distance pass of step t+1 (train_spec.cu, R32; the same
+ *     BMU log and weights as kernel 2 unless two units' exact distances
+ *     round to fp32 values closer than the certificate's margin — the
+ *     probability argument of R10),
  * 7 = kernel 6 for the steps whose neighbourhood still covers >= 70 % of
  *     the map (SOM_SPEC_COVER), then kernel 2 (two launches in one call).
  * Where kernel 2 applies on one GPU the environment variable SOM_TRAIN_SPEC
  * selects: unset or 0 = kernel 2 (default), 1 = kernel 6 for the whole
  * range, 2 = kernel 7 (needs >= 8192 prototype elements per CTA and no
- * forced mode or grid).  All give identical results. */
+ * forced mode or grid).  Kernel 8 = the NCCL step path (som_set_exchange).
+ * All follow the same arithmetic contract (R9-R11). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
 /* Kernel 6 only: number of steps of the last som_train_online call whose
@@ -211,6 +216,42 @@ som_status som_comm_mailbox_ipc(som_ctx *h, uint8_t *handle64);
 som_status som_comm_set_peers_ipc(som_ctx *h, const uint8_t *handles);
 som_status som_comm_set_peers_dev(som_ctx *h, void *const *mailboxes);
 som_status som_comm_mailbox_ptr(som_ctx *h, void **mailbox);
+
+/* ---- NCCL communicator.  som_comm_unique_id on rank 0
+ * fills a 128-byte ncclUniqueId (broadcast it to the other ranks, e.g. with
+ * torch.distributed); every rank then calls som_comm_init_nccl with its
+ * rank, the world size, the id and the shard mode.  The call is collective
+ * (ncclCommInitRank) and binds the communicator to the handle's device.
+ *   SOM_SHARD_DOCS    each rank maps / scores its own documents ("we
+ *                     assigned each document vector"); som_errors and
+ *                     som_errors_csr sum the fp64 sqrt(D1) total and the
+ *                     int64 counts (non-adjacent pairs, non-zero rows) over
+ *                     the ranks before dividing, so every rank returns QE
+ *                     and TE of the whole corpus.  Errors calls are then
+ *                     collective; a rank with no documents passes n = 0.
+ *                     Per-document outputs equal those of one GPU.
+ *   SOM_SHARD_NEURONS som_comm_init(h, rank, world) (units u = rank +
+ *                     world * l) plus the communicator, so the per-step
+ *                     winner can be exchanged with NCCL (som_set_exchange).
+ * Errors: SOM_EINVAL (bad rank/world/mode), SOM_ENCCL (NCCL failure;
+ * handle poisoned). */
+typedef enum { SOM_SHARD_DOCS = 1, SOM_SHARD_NEURONS = 2 } som_shard_mode;
+som_status som_comm_unique_id(uint8_t *id128);
+som_status som_comm_init_nccl(som_ctx *h, int32_t rank, int32_t world, const uint8_t *id128, int32_t shard_mode);
+
+/* Per-step winner exchange of neuron-sharded training (§8.E):
+ *   SOM_XCHG_MAILBOX (default) in-kernel, through the peer-memory mailboxes
+ *                    of som_comm_set_peers_* (one persistent launch);
+ *   SOM_XCHG_NCCL    the baseline: one step kernel per step (pending Eq. 1
+ *                    update + fp64 distance, one CTA per unit) followed by
+ *                    ncclAllReduce(u64 key, min) on the handle's stream,
+ *                    replayed from CUDA graphs (kernel id 8 in
+ *                    som_last_train_config).  Needs som_comm_init_nccl (any
+ *                    world, including 1).  Same results as the mailbox
+ *                    path (identical per-unit arithmetic, exact integer
+ *                    min). */
+typedef enum { SOM_XCHG_MAILBOX = 0, SOM_XCHG_NCCL = 1 } som_exchange;
+som_status som_set_exchange(som_ctx *h, int32_t mode);
 
 /* Phase trace of the register-resident training kernel (profiling aid):
  * device_buf (device memory, 148 * steps * 8 uint64, layout [CTA][step][8])
@@ -288,11 +329,14 @@ som_status som_map_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
  * inputs take EXACT_F64, or 3XTF32 once n*N*dim >= 1e10. */
 som_status som_set_map_precision(som_ctx *h, int32_t precision);
 
-/* Quantization error (R14; Table 2): mean over rows of
- * sqrt(D at the BMU), summed in fp64.  n >= 1. */
+/* Quantization error (R14; Table 2): mean over the
+ * non-zero rows of sqrt(D at the BMU), summed in fp64.
+ * n >= 1; SOM_EEMPTY when every row is zero.  Document-sharded handles
+ * (som_comm_init_nccl) reduce over the ranks (collective). */
 som_status som_qerror(som_ctx *h, const float *X, int64_t n, double *qe);
-/* Topographic error (R15; BJ:5): fraction of rows whose two best units are
- * not lattice-adjacent (g2 != 1; 0 for a 1-unit map).  n >= 1. */
+/* Topographic error (R15; BJ:5): fraction of the non-zero rows whose two
+ * best units are not lattice-adjacent (g2 != 1; 0 for a 1-unit map).
+ * n >= 1 (as som_qerror). */
 som_status som_topographic_error(som_ctx *h, const float *X, int64_t n, double *te);
 /* Both errors from one mapping pass.  qe, te nullable. */
 som_status som_errors(som_ctx *h, const float *X, int64_t n, double *qe, double *te);

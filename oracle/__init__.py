@@ -59,6 +59,9 @@ def lib():
         L.or_train_online.restype = ctypes.c_int
         L.or_train_online.argtypes = [P, i32, i32, i32, i64, P, i64, i32, f64, f64, i32,
                                       f64, f64, f64, u64, i64, i64, P, P]
+        L.or_train_online_csr.restype = ctypes.c_int
+        L.or_train_online_csr.argtypes = [P, i32, i32, i32, i64, P, P, P, i64, i32, f64, f64, i32,
+                                          f64, f64, f64, u64, i64, i64, P]
         L.or_map.restype = None
         L.or_map.argtypes = [P, i64, i64, P, i64, P, P, P, P, P]
         L.or_map_csr.restype = None
@@ -71,6 +74,14 @@ def lib():
         L.or_row_sqnorm.argtypes = [P, i64, i64, P]
         L.or_qerror_from_d1.restype = f64
         L.or_qerror_from_d1.argtypes = [P, i64]
+        L.or_qerror_masked.restype = f64
+        L.or_qerror_masked.argtypes = [P, P, i64]
+        L.or_topographic_error_masked.restype = f64
+        L.or_topographic_error_masked.argtypes = [i32, i32, i32, P, P, P, i64]
+        L.or_nonzero_rows.restype = i64
+        L.or_nonzero_rows.argtypes = [P, i64, i64, P]
+        L.or_nonzero_rows_csr.restype = i64
+        L.or_nonzero_rows_csr.argtypes = [P, P, i64, P]
         L.or_topographic_error_from_bmus.restype = f64
         L.or_topographic_error_from_bmus.argtypes = [i32, i32, i32, P, P, i64]
         L.or_umatrix.restype = None
@@ -145,9 +156,32 @@ def train_online(W, rows, cols, topo, X, epochs, alpha0, sigma0, seed,
     rc = lib().or_train_online(_p(W), rows, cols, topo, d, _p(X), n, epochs, alpha0, sigma0,
                                kind, k, sigma_min, eps, seed & (2**64 - 1), t_begin, te,
                                _p(log), _p(margins))
+    if rc == -2:
+        raise ValueError("or_train_online: EmptyData (every row is zero, S:219)")
     if rc != 0:
         raise ValueError("or_train_online: bad arguments")
     return (W, log, margins) if want_margins else (W, log)
+
+
+def train_online_csr(W, rows, cols, topo, rowptr, col, val, epochs, alpha0, sigma0, seed,
+                     kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0, eps=1e-4, t_begin=0, t_end=-1):
+    """Online SOM on CSR rows (x_t densified per step).  Returns (W', bmu_log)."""
+    W = np.array(W, dtype=np.float32, copy=True, order="C")
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    val = _f32(val)
+    n = rowptr.shape[0] - 1
+    d = W.shape[1]
+    T = epochs * n
+    te = T if t_end < 0 else t_end
+    log = np.empty(max(te - t_begin, 0), dtype=np.int32)
+    rc = lib().or_train_online_csr(_p(W), rows, cols, topo, d, _p(rowptr), _p(col), _p(val), n, epochs, alpha0,
+                                   sigma0, kind, k, sigma_min, eps, seed & (2**64 - 1), t_begin, te, _p(log))
+    if rc == -2:
+        raise ValueError("or_train_online_csr: EmptyData (every row is zero, S:219)")
+    if rc != 0:
+        raise ValueError("or_train_online_csr: bad arguments")
+    return W, log
 
 
 # --------------------------------------------------------------- mapping
@@ -215,25 +249,55 @@ def map_docs_csr(W, rowptr, col, val, want_margins=False):
 from .upstream import linear_init, map_geometry, pca_top2  # noqa: E402,F401
 
 
-def qerror_from_d1(d1) -> float:
+def nonzero_rows(X):
+    """Indices of the rows of X holding a non-zero value."""
+    X = _f32(X)
+    idx = np.empty(X.shape[0], np.int64)
+    m = lib().or_nonzero_rows(_p(X), X.shape[0], X.shape[1], _p(idx))
+    return idx[:m]
+
+
+def nonzero_rows_csr(rowptr, val):
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    val = _f32(val)
+    idx = np.empty(rowptr.shape[0] - 1, np.int64)
+    m = lib().or_nonzero_rows_csr(_p(rowptr), _p(val), rowptr.shape[0] - 1, _p(idx))
+    return idx[:m]
+
+
+def keep_mask(n, nz_idx):
+    keep = np.zeros(n, np.uint8)
+    keep[nz_idx] = 1
+    return keep
+
+
+def qerror_from_d1(d1, keep=None) -> float:
+    """QE (R14) over the rows with keep[i] != 0 (all rows if keep is None):
+    zero rows are not scored."""
     d1 = _f32(d1)
-    return float(lib().or_qerror_from_d1(_p(d1), d1.shape[0]))
+    if keep is None:
+        return float(lib().or_qerror_from_d1(_p(d1), d1.shape[0]))
+    keep = np.ascontiguousarray(keep, np.uint8)
+    return float(lib().or_qerror_masked(_p(d1), _p(keep), d1.shape[0]))
 
 
 def qerror(W, X) -> float:
     _, _, d1 = map_docs(W, X)
-    return qerror_from_d1(d1)
+    return qerror_from_d1(d1, keep_mask(X.shape[0], nonzero_rows(X)))
 
 
-def topographic_error_from_bmus(rows, cols, topo, b1, b2) -> float:
+def topographic_error_from_bmus(rows, cols, topo, b1, b2, keep=None) -> float:
     b1 = np.ascontiguousarray(b1, np.int32)
     b2 = np.ascontiguousarray(b2, np.int32)
-    return float(lib().or_topographic_error_from_bmus(rows, cols, topo, _p(b1), _p(b2), b1.shape[0]))
+    if keep is None:
+        return float(lib().or_topographic_error_from_bmus(rows, cols, topo, _p(b1), _p(b2), b1.shape[0]))
+    keep = np.ascontiguousarray(keep, np.uint8)
+    return float(lib().or_topographic_error_masked(rows, cols, topo, _p(b1), _p(b2), _p(keep), b1.shape[0]))
 
 
 def topographic_error(W, rows, cols, topo, X) -> float:
     b1, b2, _ = map_docs(W, X)
-    return topographic_error_from_bmus(rows, cols, topo, b1, b2)
+    return topographic_error_from_bmus(rows, cols, topo, b1, b2, keep_mask(X.shape[0], nonzero_rows(X)))
 
 
 def umatrix(W, rows, cols, topo):

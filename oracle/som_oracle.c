@@ -168,6 +168,34 @@ void or_update(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t d,
  * adapt.  T = epochs * n (R7).  Steps
  * t in [t_begin, t_end) are run; bmu_log[t - t_begin] = c_t (nullable);
  * margin_log likewise (nullable).  Returns 0, or -1 on bad arguments. */
+/* Zero rows ("All-zero document rows after filtering are retained
+ * but excluded from training sample draws"): the indices of
+ * the rows holding at least one non-zero value, ascending, into idx
+ * (nullable); returns their count. */
+int64_t or_nonzero_rows(const float *X, int64_t n, int64_t d, int64_t *idx)
+{
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int nz = 0;
+        for (int64_t k = 0; k < d && !nz; ++k) nz = X[i * d + k] != 0.0f;
+        if (nz) { if (idx) idx[m] = i; ++m; }
+    }
+    return m;
+}
+
+/* The same for CSR rows: a row is zero when it stores no non-zero value
+ * (explicit zeros, e.g. idf-0 terms of R28, do not count). */
+int64_t or_nonzero_rows_csr(const int64_t *rowptr, const float *val, int64_t n, int64_t *idx)
+{
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int nz = 0;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1] && !nz; ++p) nz = val[p] != 0.0f;
+        if (nz) { if (idx) idx[m] = i; ++m; }
+    }
+    return m;
+}
+
 int or_train_online(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t d,
                     const float *X, int64_t n, int32_t epochs,
                     double alpha0, double sigma0, int32_t decay_kind, double k,
@@ -178,9 +206,17 @@ int or_train_online(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t 
     int64_t T = (int64_t)epochs * n;
     if (t_end < 0) t_end = T;
     if (t_begin < 0 || t_begin > t_end || t_end > T) return -1;
+    if (t_end == t_begin) return 0;
     int64_t N = (int64_t)rows * cols;
+    /* R8 + S:218: draws are uniform over the non-zero rows only (the j-th
+     * non-zero row for draw j); T = epochs * n stays the step count (R7).
+     * Without zero rows this is the plain sampler over [0, n). */
+    int64_t *nzr = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    if (!nzr) return -1;
+    int64_t m = or_nonzero_rows(X, n, d, nzr);
+    if (m == 0) { free(nzr); return -2; }   /* EmptyData */
     for (int64_t t = t_begin; t < t_end; ++t) {
-        int64_t i = or_sample_index(seed, t, n);
+        int64_t i = nzr[or_sample_index(seed, t, m)];
         const float *x = X + i * d;
         double margin;
         int64_t c = or_bmu(W, N, d, x, NULL, &margin);
@@ -191,6 +227,42 @@ int or_train_online(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t 
         if (bmu_log) bmu_log[t - t_begin] = (int32_t)c;
         if (margin_log) margin_log[t - t_begin] = margin;
     }
+    free(nzr);
+    return 0;
+}
+
+/* The same online SOM on CSR rows (the sparse TF-IDF DTM of P:148-154):
+ * x_t is densified into a zeroed d-vector and the step is or_bmu +
+ * or_update exactly as above.  Lets the oracle follow corpora whose dense
+ * copy would not fit (c4: 200k x 20k). */
+int or_train_online_csr(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t d,
+                        const int64_t *rowptr, const int32_t *col, const float *val,
+                        int64_t n, int32_t epochs, double alpha0, double sigma0,
+                        int32_t decay_kind, double k, double sigma_min, double eps,
+                        uint64_t seed, int64_t t_begin, int64_t t_end, int32_t *bmu_log)
+{
+    int64_t T = (int64_t)epochs * n;
+    if (t_end < 0) t_end = T;
+    if (t_begin < 0 || t_begin > t_end || t_end > T) return -1;
+    if (t_end == t_begin) return 0;
+    int64_t N = (int64_t)rows * cols;
+    int64_t *nzr = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    float *x = (float *)calloc((size_t)d, sizeof(float));
+    if (!nzr || !x) { free(nzr); free(x); return -1; }
+    int64_t m = or_nonzero_rows_csr(rowptr, val, n, nzr);
+    if (m == 0) { free(nzr); free(x); return -2; }
+    for (int64_t t = t_begin; t < t_end; ++t) {
+        int64_t i = nzr[or_sample_index(seed, t, m)];
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) x[col[p]] = val[p];
+        int64_t c = or_bmu(W, N, d, x, NULL, NULL);
+        double alpha, sigma, r2;
+        or_schedule(decay_kind, k, t, T, alpha0, sigma0, sigma_min, eps, &alpha, &sigma, &r2);
+        or_update(W, rows, cols, topo, d, x, c, alpha, sigma, r2);
+        if (bmu_log) bmu_log[t - t_begin] = (int32_t)c;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) x[col[p]] = 0.0f;
+    }
+    free(nzr);
+    free(x);
     return 0;
 }
 
@@ -358,6 +430,20 @@ double or_qerror_from_d1(const float *d1, int64_t n)
     return s / (double)n;
 }
 
+/* S:227 "mean over nonzero rows": keep[i] != 0 marks the rows that
+ * count; NAN when none does (EmptyData). */
+double or_qerror_masked(const float *d1, const uint8_t *keep, int64_t n)
+{
+    double s = 0.0;
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (!keep[i]) continue;
+        s += sqrt((double)d1[i]);
+        ++m;
+    }
+    return m ? s / (double)m : NAN;
+}
+
 /* R13, R15 (BJ:5; not in the paper): topographic error = fraction of rows
  * whose first and second BMUs are not lattice-adjacent (g2 != 1).
  * A 1-unit map has no second BMU: TE := 0 (R23). */
@@ -371,6 +457,21 @@ double or_topographic_error_from_bmus(int32_t rows, int32_t cols, int32_t topo,
         if (or_lattice_g2(rows, cols, topo, bmu1[i], bmu2[i]) != 1.0) ++bad;
     }
     return (double)bad / (double)n;
+}
+
+/* TE over the rows keep[i] != 0 only (zero rows are scored like QE). */
+double or_topographic_error_masked(int32_t rows, int32_t cols, int32_t topo,
+                                   const int32_t *bmu1, const int32_t *bmu2,
+                                   const uint8_t *keep, int64_t n)
+{
+    int64_t bad = 0, m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (!keep[i]) continue;
+        ++m;
+        if (bmu2[i] < 0) continue;
+        if (or_lattice_g2(rows, cols, topo, bmu1[i], bmu2[i]) != 1.0) ++bad;
+    }
+    return m ? (double)bad / (double)m : NAN;
 }
 
 /* -------------------------------------------------------------- U-matrix */

@@ -13,8 +13,11 @@ constexpr int kRedThreads = 256;
 // best units are not adjacent (g2 != 1, R15) over a contiguous row range.
 // Pass 2 (one CTA) adds the per-CTA partials in index order, so the result
 // does not depend on scheduling.
-__global__ void errors_partial_kernel(const int32_t* bmu1, const int32_t* bmu2, const float* d2, int64_t n,
-                                      int cols, int topo, double* partial, unsigned long long* partial_cnt) {
+// Zero rows (keep[i] == 0; keep nullable = every row) are not scored
+// (S:227); the count of scored rows comes from the host.
+__global__ void errors_partial_kernel(const int32_t* bmu1, const int32_t* bmu2, const float* d2,
+                                      const uint8_t* keep, int64_t n, int cols, int topo, double* partial,
+                                      unsigned long long* partial_cnt) {
     __shared__ double ssum[kRedThreads / 32];
     __shared__ unsigned long long scnt[kRedThreads / 32];
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -23,6 +26,7 @@ __global__ void errors_partial_kernel(const int32_t* bmu1, const int32_t* bmu2, 
     double s = 0.0;
     unsigned long long c = 0;
     for (int64_t i = r0 + threadIdx.x; i < r1; i += kRedThreads) {
+        if (keep && !keep[i]) continue;
         s += sqrt((double)d2[i]);
         const int b2 = bmu2[i];
         if (b2 >= 0 && lattice_g2(cols, topo, bmu1[i], b2) != 1.0) ++c;
@@ -99,11 +103,12 @@ __global__ void gather_rows_kernel(const float* X, const int64_t* idx, int dim, 
 
 }  // namespace
 
-cudaError_t launch_errors(const int32_t* bmu1, const int32_t* bmu2, const float* d2, int64_t n, int rows,
-                          int cols, int topo, double* partial, unsigned long long* partial_cnt, int nblocks,
+cudaError_t launch_errors(const int32_t* bmu1, const int32_t* bmu2, const float* d2, const uint8_t* keep, int64_t n,
+                          int rows, int cols, int topo, double* partial, unsigned long long* partial_cnt, int nblocks,
                           double* out_qe_sum, unsigned long long* out_bad, cudaStream_t st) {
     (void)rows;
-    errors_partial_kernel<<<nblocks, kRedThreads, 0, st>>>(bmu1, bmu2, d2, n, cols, topo, partial, partial_cnt);
+    errors_partial_kernel<<<nblocks, kRedThreads, 0, st>>>(bmu1, bmu2, d2, keep, n, cols, topo, partial,
+                                                           partial_cnt);
     errors_final_kernel<<<1, 32, 0, st>>>(partial, partial_cnt, nblocks, out_qe_sum, out_bad);
     return cudaGetLastError();
 }

@@ -97,8 +97,12 @@ som_status stage_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, cons
                      CsrIn* out) {
     if (!rowptr || !col || !val) return fail(SOM_EINVAL, "null CSR array");
     int64_t nnz = 0;
-    if (is_device_ptr(rowptr)) CK(cudaMemcpy(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    else nnz = rowptr[n];
+    if (is_device_ptr(rowptr)) {   // on the handle's stream: the caller may have produced rowptr on it
+        CK(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    } else {
+        nnz = rowptr[n];
+    }
     if (nnz < 0) return fail(SOM_EINVAL, "rowptr[n] < 0");
     const void *rpd, *cd, *vd;
     som_status st = stage_in(h, h->xin, rowptr, sizeof(int64_t) * (size_t)(n + 1), &rpd);
@@ -122,8 +126,30 @@ som_status stage_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, cons
     return SOM_OK;
 }
 
+som_status scan_rows(som_ctx* h, const float* Xd, const CsrIn* csr, int64_t n, int64_t* m, const int64_t** list) {
+    CK(h->rflags.ensure((size_t)std::max<int64_t>(n, 1), h->stream));
+    uint8_t* flags = (uint8_t*)h->rflags.p;
+    if (csr) CK(launch_row_flags_csr(csr->rowptr, csr->val, n, flags, h->stream));
+    else CK(launch_row_flags_dense(Xd, n, h->dim, flags, h->stream));
+    const size_t tb = select_rows_temp_bytes(n);
+    const size_t idx_bytes = sizeof(int64_t) * ((size_t)n + 1);
+    CK(h->rmap.ensure(idx_bytes + 256 + tb, h->stream));
+    int64_t* idx = (int64_t*)h->rmap.p;
+    int64_t* cnt = idx + n;
+    void* temp = (char*)h->rmap.p + ((idx_bytes + 255) & ~(size_t)255);
+    CK(launch_select_rows(flags, n, idx, cnt, temp, tb, h->stream));
+    int64_t c = 0;
+    CK(cudaMemcpyAsync(&c, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    *m = c;
+    if (list) *list = c < n ? idx : nullptr;
+    return SOM_OK;
+}
+
 }  // namespace host
 }  // namespace som
+
+void som_comm_release(som_ctx* h);
 
 namespace {
 uint64_t mulhi_host(uint64_t a, uint64_t b) { return (uint64_t)(((unsigned __int128)a * b) >> 64); }
@@ -191,8 +217,10 @@ void som_destroy(som_ctx* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    som_comm_release(h);
     for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
-                      &h->utab, &h->wsplit, &h->xsplit, &h->wt64, &h->bbuf, &h->bS, &h->bnum, &h->up, &h->up2})
+                      &h->utab, &h->wsplit, &h->xsplit, &h->wt64, &h->bbuf, &h->bS, &h->bnum, &h->up, &h->up2,
+                      &h->rflags, &h->rmap, &h->nstep})
         b->release();
     if (h->W) cudaFree(h->W);
     for (int p = 0; p < kMaxRanks; ++p)

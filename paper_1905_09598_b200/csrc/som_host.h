@@ -96,6 +96,16 @@ struct som_ctx {
     DevBuf bS, bnum; // batch SOM: per-BMU sums S and H S (fp64, N x (d+1))
     DevBuf up, up2;  // upstream steps (TF-IDF / PCA scratch)
     DevBuf wt64;     // sparse mapping: W^T fp64 or fp32 (dim x Np) | |W|^2 fp64 (N)
+    DevBuf rflags;   // zero-row flags (n bytes, 1 = the row holds a non-zero value)
+    DevBuf rmap;     // ascending list of the non-zero rows (int64) | count | select temp
+    // NCCL communicator (som_comm_init_nccl): document sharding reduces the
+    // error sums over it; neuron sharding can exchange the per-step winner
+    // through it (SOM_XCHG_NCCL) instead of the peer-memory mailboxes
+    void* nccl = nullptr;   // ncclComm_t
+    int shard_mode = 0;     // 0 none, SOM_SHARD_DOCS, SOM_SHARD_NEURONS
+    int nccl_rank = 0, nccl_world = 1;
+    int xchg_mode = 0;      // SOM_XCHG_MAILBOX / SOM_XCHG_NCCL
+    DevBuf nstep;           // NCCL step path: keys [3] u64 | reduce scratch
     bool wt_valid = false, wt_f32 = false, wt_nonneg = false;
     int wt_J = 0;
     // decay-table cache
@@ -154,6 +164,16 @@ void invalidate_w_caches(som_ctx* h);
 void fill_decay(double* out, int64_t t0, int64_t t1, int64_t T, int kind, double k);
 som_status ensure_decay_table(som_ctx* h, int64_t T, int kind, double k, int64_t t0, int64_t t1);
 som_status stage_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n, CsrIn* out);
+// zero rows: flags of the n rows of Xd (or csr) into
+// h->rflags, *m = number of non-zero rows; with list != NULL, *list = the
+// ascending non-zero rows (h->rmap) when some row is zero, else NULL
+som_status scan_rows(som_ctx* h, const float* Xd, const CsrIn* csr, int64_t n, int64_t* m, const int64_t** list);
+// document sharding over NCCL: in-place sum of (f64 s, i64 c[2]) over the
+// communicator (no-op without one)
+som_status doc_allreduce(som_ctx* h, double* s, int64_t* c);
+// som_comm.cu: step-at-a-time training with one NCCL u64-min all-reduce per
+// step (a: TrainArgs of the call; launches: kernels + collectives issued)
+som_status train_nccl_steps(som_ctx* h, const TrainArgs& a, int* launches);
 // som_map_api.cu
 bool use_tc(const som_ctx* h, int64_t n);
 int csr_path(const som_ctx* h, const CsrIn& csr, int64_t n);
@@ -162,7 +182,8 @@ som_status map_exact_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, in
 som_status map_csr_dev(som_ctx* h, const CsrIn& csr, int64_t n, int32_t* b1, int32_t* b2, float* d2, int* launches);
 som_status stage_outputs(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2, bool need_all, OutStage& o);
 som_status copy_back(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float* d2, const OutStage& o);
-som_status finish_errors(som_ctx* h, int64_t n, const OutStage& o, int launches, double* qe, double* te);
+som_status finish_errors(som_ctx* h, int64_t n, const OutStage& o, int launches, double* qe, double* te, int64_t m);
+bool doc_sharded(const som_ctx* h);
 
 }  // namespace host
 }  // namespace som

@@ -30,6 +30,11 @@ struct TrainArgs {
     int64_t t0, t1;            // step range
     uint64_t seed;
     const double* f_tab;       // decay factor f_t for t in [t0, t1)
+    // zero rows: draws go to rowmap[i] for i uniform over
+    // [0, n_draw) (the non-zero rows, ascending); rowmap = NULL: no zero
+    // row, draws uniform over [0, n)
+    const int64_t* rowmap;
+    int64_t n_draw;
     double alpha0, sigma0, sigma_min, ln_inv_eps;
     int cutoff_on;             // 0: every unit adapts (eps = 0)
     unsigned long long* xchg;  // [2][G] per-CTA BMU candidate slots
@@ -144,6 +149,12 @@ inline cudaError_t launch_persistent(const void* fn, const TrainArgs& a, int thr
     if (e != cudaSuccess) return e;
     if (a.G > sms * per_sm) return cudaErrorCooperativeLaunchTooLarge;
     return cudaLaunchKernel(fn, dim3(a.G), dim3(threads), params, smem, st);
+}
+
+// R8 + S:218: the row drawn at step t (uniform over the non-zero rows)
+__device__ __forceinline__ int64_t train_row(const TrainArgs& a, int64_t t) {
+    if (a.rowmap) return __ldg(a.rowmap + sample_at(a.seed, t, a.n_draw));
+    return sample_at(a.seed, t, a.n);
 }
 
 // global unit index of local unit l
@@ -295,11 +306,22 @@ cudaError_t launch_dense_fill(const float* X, int64_t m, int d, const int64_t* r
 cudaError_t launch_densify(const int64_t* rowptr, const int32_t* col, const float* val,
                            int64_t r0, int64_t nrows, int dim, float* out, cudaStream_t st);
 
-// QE / TE partial sums (deterministic two-pass) and U-matrix.
-cudaError_t launch_errors(const int32_t* bmu1, const int32_t* bmu2, const float* d2,
+// QE / TE partial sums (deterministic two-pass) over the rows with
+// keep[i] != 0 (keep nullable = every row), and U-matrix.
+cudaError_t launch_errors(const int32_t* bmu1, const int32_t* bmu2, const float* d2, const uint8_t* keep,
                           int64_t n, int rows, int cols, int topo, double* partial,
                           unsigned long long* partial_cnt, int nblocks, double* out_qe_sum,
                           unsigned long long* out_bad, cudaStream_t st);
+
+// zero rows (rows.cu): flags[i] = row i holds a non-zero value; the
+// ascending list of flagged rows (CUB select, temp from
+// select_rows_temp_bytes) and its length (device int64)
+cudaError_t launch_row_flags_dense(const float* X, int64_t n, int dim, uint8_t* flags, cudaStream_t st);
+cudaError_t launch_row_flags_csr(const int64_t* rowptr, const float* val, int64_t n, uint8_t* flags,
+                                 cudaStream_t st);
+size_t select_rows_temp_bytes(int64_t n);
+cudaError_t launch_select_rows(const uint8_t* flags, int64_t n, int64_t* idx, int64_t* count, void* temp,
+                               size_t temp_bytes, cudaStream_t st);
 cudaError_t launch_umatrix(const float* W, int rows, int cols, int topo, int dim, float* U,
                            cudaStream_t st);
 cudaError_t launch_gather_rows(const float* X, const int64_t* idx, int N, int dim, float* W,

@@ -244,23 +244,40 @@ som_status copy_back(som_ctx* h, int64_t n, int32_t* bmu1, int32_t* bmu2, float*
 
 // QE/TE sums from device mapping outputs (deterministic two-pass), then
 // the call's timing; ev0 was recorded before the mapping.
-som_status finish_errors(som_ctx* h, int64_t n, const OutStage& o, int launches, double* qe, double* te) {
-    const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
-    CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2), h->stream));
-    double* partial = (double*)h->red.p;
-    unsigned long long* pcnt = (unsigned long long*)(partial + nb);
-    double* osum = (double*)(pcnt + nb);
-    unsigned long long* obad = (unsigned long long*)(osum + 1);
-    CK(launch_errors(o.b1, o.b2, o.d2, n, h->rows, h->cols, h->topo, partial, pcnt, nb, osum, obad, h->stream));
-    launches += 2;
-    CK(cudaEventRecord(h->ev1, h->stream));
+// Zero rows are not scored: the flags of scan_rows (called
+// by the entry point, h->rflags) select the rows, m = their count.  With
+// document sharding (som_comm_init_nccl, SOM_SHARD_DOCS) the fp64 sum and
+// the integer counts are summed over the ranks before the division, so
+// every rank returns the errors of the whole corpus.
+bool doc_sharded(const som_ctx* h) { return h->nccl && h->shard_mode == SOM_SHARD_DOCS; }
+
+som_status finish_errors(som_ctx* h, int64_t n, const OutStage& o, int launches, double* qe, double* te, int64_t m) {
     double sum = 0;
     unsigned long long bad = 0;
-    CK(cudaMemcpyAsync(&sum, osum, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(&bad, obad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    if (n > 0) {
+        const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 4095) / 4096), 4 * (int64_t)h->sm_count);
+        CK(h->red.ensure((sizeof(double) + sizeof(unsigned long long)) * ((size_t)nb + 2), h->stream));
+        double* partial = (double*)h->red.p;
+        unsigned long long* pcnt = (unsigned long long*)(partial + nb);
+        double* osum = (double*)(pcnt + nb);
+        unsigned long long* obad = (unsigned long long*)(osum + 1);
+        const uint8_t* keep = m < n ? (const uint8_t*)h->rflags.p : nullptr;
+        CK(launch_errors(o.b1, o.b2, o.d2, keep, n, h->rows, h->cols, h->topo, partial, pcnt, nb, osum, obad,
+                         h->stream));
+        launches += 2;
+        CK(cudaMemcpyAsync(&sum, osum, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(&bad, obad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(cudaEventRecord(h->ev1, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    if (qe) *qe = sum / (double)n;
-    if (te) *te = (double)bad / (double)n;
+    int64_t cnt[2] = {(int64_t)bad, m};
+    if (doc_sharded(h)) {
+        som_status st = doc_allreduce(h, &sum, cnt);
+        if (st) return st;
+    }
+    if (cnt[1] == 0) return fail(SOM_EEMPTY, "every row is zero: no row to score (S:227)");
+    if (qe) *qe = sum / (double)cnt[1];
+    if (te) *te = (double)cnt[0] / (double)cnt[1];
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_ms = ms; h->last_units = n; h->last_launches = launches;
@@ -326,7 +343,13 @@ som_status som_errors_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col,
     CHECK_HANDLE(h);
     if (h->world > 1)
         return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
-    if (n < 1) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    if (n < 0) return fail(SOM_EINVAL, "n < 0");
+    if (n < 1 && !doc_sharded(h)) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    if (n == 0) {   // document sharding: an empty shard still joins the reduction
+        OutStage o;
+        CK(cudaEventRecord(h->ev0, h->stream));
+        return finish_errors(h, 0, o, 0, qe, te, 0);
+    }
     CsrIn csr{};
     som_status st = stage_csr(h, rowptr, col, val, n, &csr);
     if (st) return st;
@@ -335,15 +358,23 @@ som_status som_errors_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col,
     int launches = 0;
     CK(cudaEventRecord(h->ev0, h->stream));
     if ((st = map_csr_dev(h, csr, n, o.b1, o.b2, o.d2, &launches))) return st;
-    return finish_errors(h, n, o, launches, qe, te);
+    int64_t m = 0;
+    if ((st = scan_rows(h, nullptr, &csr, n, &m, nullptr))) return st;
+    return finish_errors(h, n, o, launches + 2, qe, te, m);
 }
 
 som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double* te) {
     CHECK_HANDLE(h);
     if (h->world > 1)
         return fail(SOM_EUNSUPPORTED, "neuron-sharded handle: gather W into an unsharded handle to map / score");
-    if (!X) return fail(SOM_EINVAL, "null X");
-    if (n < 1) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    if (n < 0) return fail(SOM_EINVAL, "n < 0");
+    if (n < 1 && !doc_sharded(h)) return fail(SOM_EEMPTY, "n = 0: errors need data");
+    if (!X && n > 0) return fail(SOM_EINVAL, "null X");
+    if (n == 0) {   // document sharding: an empty shard still joins the reduction
+        OutStage o;
+        CK(cudaEventRecord(h->ev0, h->stream));
+        return finish_errors(h, 0, o, 0, qe, te, 0);
+    }
     const void* Xd = nullptr;
     som_status st = stage_in(h, h->xin, X, sizeof(float) * (size_t)n * h->dim, &Xd);
     if (st) return st;
@@ -352,7 +383,9 @@ som_status som_errors(som_ctx* h, const float* X, int64_t n, double* qe, double*
     int launches = 0;
     CK(cudaEventRecord(h->ev0, h->stream));
     if ((st = map_dense_dev(h, (const float*)Xd, n, o.b1, o.b2, o.d2, &launches))) return st;
-    return finish_errors(h, n, o, launches, qe, te);
+    int64_t m = 0;
+    if ((st = scan_rows(h, (const float*)Xd, nullptr, n, &m, nullptr))) return st;
+    return finish_errors(h, n, o, launches + 2, qe, te, m);
 }
 
 som_status som_qerror(som_ctx* h, const float* X, int64_t n, double* qe) {

@@ -78,11 +78,49 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     som_status st = SOM_OK;
     if ((st = ensure_decay_table(h, T, sd.kind, sd.k, t_begin, t_end))) return st;
 
+    // zero rows are never drawn: the draws go to the list of
+    // non-zero rows when some row is zero (R8 over that list)
+    int64_t n_draw = 0;
+    const int64_t* rowmap = nullptr;
+    if ((st = scan_rows(h, (const float*)Xd, csr, n, &n_draw, &rowmap))) return st;
+    if (n_draw == 0) return fail(SOM_EEMPTY, "every row is zero: nothing to draw (S:219)");
+
     TrainArgs a{};
     a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
+    a.rowmap = rowmap; a.n_draw = n_draw;
     a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->NL;
     a.rank = h->rank; a.world = h->world;
     for (int p = 0; p < kMaxRanks; ++p) a.mail[p] = h->peer_mail[p];
+    if (h->xchg_mode == SOM_XCHG_NCCL) {
+        // step-at-a-time path, winner exchanged by ncclAllReduce (som_comm.cu)
+        a.t0 = t_begin; a.t1 = t_end; a.seed = seed;
+        a.f_tab = (const double*)h->ftab.p;
+        a.alpha0 = alpha0; a.sigma0 = sigma0; a.sigma_min = sd.sigma_min;
+        a.cutoff_on = sd.cutoff > 0.0;
+        a.ln_inv_eps = sd.cutoff > 0.0 ? std::log(1.0 / sd.cutoff) : 0.0;
+        a.G = h->NL;
+        if (csr) {   // the step kernel reads dense rows
+            CK(h->dense.ensure(sizeof(float) * (size_t)n * h->dim, h->stream));
+            CK(launch_densify(csr->rowptr, csr->col, csr->val, 0, n, h->dim, (float*)h->dense.p, h->stream));
+            a.X = (const float*)h->dense.p;
+        }
+        const int64_t steps = t_end - t_begin;
+        const bool log_dev = bmu_log && is_device_ptr(bmu_log);
+        if (bmu_log && !log_dev) CK(h->log.ensure(sizeof(int32_t) * (size_t)steps, h->stream));
+        a.bmu_log = bmu_log ? (log_dev ? bmu_log : (int32_t*)h->log.p) : nullptr;
+        int launches = 0;
+        CK(cudaEventRecord(h->ev0, h->stream));
+        if ((st = train_nccl_steps(h, a, &launches))) return st;
+        CK(cudaEventRecord(h->ev1, h->stream));
+        if (bmu_log && !log_dev)
+            CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        h->last_ms = ms; h->last_units = steps; h->last_launches = launches;
+        h->last_grid = a.G; h->last_kernel = 8;
+        return SOM_OK;
+    }
     if (h->world > 1) {
         for (int p = 0; p < h->world; ++p)
             if (!h->peer_mail[p]) return fail(SOM_ESTATE, "neuron sharding: peer mailboxes not set (som_comm_set_peers_*)");
@@ -271,7 +309,12 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // W streamed from global memory every step: keep it resident in L2 with a
     // persisting access-policy window (random X rows stream past it), undone
     // after the launch so the caller's stream is left as it was.
+    // The caller's persisting-L2 limit and the stream's window are saved and
+    // restored afterwards; the persisting lines are demoted only if no
+    // persisting set-aside existed before the call (nobody else uses it).
     bool l2_window = false;
+    size_t prev_persist = 0;
+    cudaStreamAttrValue prev_win{};
     const char* nowin = std::getenv("SOM_NO_L2_WINDOW");
     if (!(nowin && std::atoi(nowin)) && !use_reg && !a.w_smem && (!use_small || small_rounds(a.S, h->dim) > 4)) {
         int max_persist = 0, max_window = 0;
@@ -287,7 +330,10 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         if (max_persist > 0 && max_window > 0 && wbytes <= (size_t)l2_bytes) {
             const size_t win = std::min(wbytes, (size_t)max_window);
             const size_t keep = std::min(win, (size_t)max_persist);
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep) == cudaSuccess) {
+            const bool saved = cudaDeviceGetLimit(&prev_persist, cudaLimitPersistingL2CacheSize) == cudaSuccess &&
+                               cudaStreamGetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &prev_win) ==
+                                   cudaSuccess;
+            if (saved && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::max(keep, prev_persist)) == cudaSuccess) {
                 cudaStreamAttrValue at{};
                 at.accessPolicyWindow.base_ptr = h->W;
                 at.accessPolicyWindow.num_bytes = win;
@@ -328,10 +374,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
-    if (l2_window) {   // later launches on the caller's stream get no window
-        cudaStreamAttrValue at{};
-        at.accessPolicyWindow.num_bytes = 0;
-        cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &at);
+    if (l2_window) {   // later launches on the stream get the caller's window back
+        cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &prev_win);
         cudaGetLastError();
     }
     h->last_grid = a.G;
@@ -339,9 +383,9 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    if (l2_window) {   // the kernel is done: demote its persisting lines and release the set-aside L2
-        cudaCtxResetPersistingL2Cache();
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    if (l2_window) {   // the kernel is done: demote its persisting lines, restore the set-aside
+        if (prev_persist == 0) cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_persist);
         cudaGetLastError();
     }
     unsigned abort_flag = 0;

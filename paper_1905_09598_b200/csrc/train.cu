@@ -56,7 +56,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int S, int dimp, int 
 
 // Stage x_t = X[i_t] into one ring slot (cp.async; caller commits/waits).
 __device__ __forceinline__ void stage_x(const TrainArgs& a, float* dst, int64_t t) {
-    const int64_t i = sample_at(a.seed, t, a.n);
+    const int64_t i = train_row(a, t);
     const float* src = a.X + i * (int64_t)a.dim;
     if (a.x_vec4) {
         const int d4 = a.dim >> 2;

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_kernel(const TrainArgs a)
     for (int j = 0; j < KJ; ++j) valid[j] = threadIdx.x + j * NT < d4;
 
     auto bounds = [&](int64_t t) {   // CSR range of sample i_t
-        const int64_t i = sample_at(a.seed, t, a.n);
+        const int64_t i = train_row(a, t);
         nb[t % 3][0] = a.rowptr[i];
         nb[t % 3][1] = a.rowptr[i + 1];
     };
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
     for (int j = 0; j < KJ; ++j) valid[j] = threadIdx.x + j * NT < d4;
 
     auto bounds = [&](int64_t t) {
-        const int64_t i = sample_at(a.seed, t, a.n);
+        const int64_t i = train_row(a, t);
         nb[t % 3][0] = a.rowptr[i];
         nb[t % 3][1] = a.rowptr[i + 1];
     };

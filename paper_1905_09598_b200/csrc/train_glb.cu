@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_glb_kernel(const TrainArgs a)
 
     auto stage = [&](int64_t t) {   // x_t -> ring[t & 1] (cp.async, own chunks)
         if (t < a.t1) {
-            const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
+            const float4* src = reinterpret_cast<const float4*>(a.X + train_row(a, t) * (int64_t)a.dim);
             float4* dst = ring4 + (size_t)(t & 1) * d4;
 #pragma unroll
             for (int j = 0; j < KJ; ++j)
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_tma_kernel(const TrainArgs a,
 
     auto stage = [&](int64_t t) {
         if (t < a.t1) {
-            const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
+            const float4* src = reinterpret_cast<const float4*>(a.X + train_row(a, t) * (int64_t)a.dim);
 #pragma unroll
             for (int j = 0; j < KJ; ++j)
                 if (valid[j]) cp_async16(xs4 + threadIdx.x + j * NT, src + threadIdx.x + j * NT);

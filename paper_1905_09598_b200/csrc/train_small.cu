@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_small_kernel(const TrainArgs 
     // x ring: threads 0..d4-1 stage whole rows with cp.async one step ahead
     auto issue_x = [&](int64_t t) {
         if (threadIdx.x < d4 && t < a.t1) {
-            const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
+            const float4* src = reinterpret_cast<const float4*>(a.X + train_row(a, t) * (int64_t)a.dim);
             cp_async16((void*)(ring4 + (size_t)(t % 3) * d4 + threadIdx.x), src + threadIdx.x);
             cp_async_commit();
         }

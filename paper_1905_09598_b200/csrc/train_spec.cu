@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_spec_kernel(const TrainArgs a
 
     auto issue_x = [&](int64_t t) {
         if (t < a.t1) {
-            const float4* src = reinterpret_cast<const float4*>(a.X + sample_at(a.seed, t, a.n) * (int64_t)a.dim);
+            const float4* src = reinterpret_cast<const float4*>(a.X + train_row(a, t) * (int64_t)a.dim);
             float4* dst = ring4 + (size_t)(t % 3) * d4;
 #pragma unroll
             for (int j = 0; j < KJ; ++j)

@@ -22,6 +22,8 @@ SOM_RECT, SOM_HEX = 0, 1
 SOM_DECAY_GAUSSIAN, SOM_DECAY_LINEAR, SOM_DECAY_EXP = 0, 1, 2
 SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32, SOM_MAP_SPARSE_F64 = 0, 1, 2, 3
 SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL, SOM_TRAIN_W_REGISTERS = 0, 1, 2, 3
+SOM_SHARD_DOCS, SOM_SHARD_NEURONS = 1, 2
+SOM_XCHG_MAILBOX, SOM_XCHG_NCCL = 0, 1
 
 _STATUS = {0: "SOM_OK", 1: "SOM_EINVAL", 2: "SOM_EDIM", 3: "SOM_EEMPTY", 4: "SOM_ENOMEM", 5: "SOM_ECUDA",
            6: "SOM_ENCCL", 7: "SOM_ESTATE", 8: "SOM_EUNSUPPORTED"}
@@ -47,7 +49,8 @@ EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights
            "som_init_linear", "som_map_geometry",
            "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
-           "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr"]
+           "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr",
+           "som_comm_unique_id", "som_comm_init_nccl", "som_set_exchange"]
 
 
 def lib():
@@ -95,6 +98,9 @@ def lib():
         "som_comm_set_peers_ipc": [P, P],
         "som_comm_set_peers_dev": [P, P],
         "som_comm_mailbox_ptr": [P, P],
+        "som_comm_unique_id": [P],
+        "som_comm_init_nccl": [P, i32, i32, P, i32],
+        "som_set_exchange": [P, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -113,6 +119,37 @@ def lib():
 def _check(st: int):
     if st != SOM_OK:
         raise SomError(st, lib().som_last_error().decode())
+
+
+# (rows*cols, dim) of every live handle, for the size checks below (the C
+# ABI takes plain pointers and cannot see buffer sizes)
+_dims: dict[int, tuple[int, int]] = {}
+
+
+def _numel(a) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _need(a, count: int, what: str):
+    """SOM_EDIM unless a holds at least `count` elements (None passes)."""
+    if a is not None and _numel(a) < count:
+        raise SomError(SOM_EDIM, f"{what}: {_numel(a)} elements, need {count}")
+
+
+def _check_rows(h, X, n: int, what: str = "X"):
+    """X must be (>= n, dim) or hold >= n * dim elements."""
+    if X is None or n <= 0:
+        return
+    d = _dims.get(_hv(h))
+    if d is None:
+        return
+    if getattr(X, "ndim", 1) == 2 and X.shape[1] != d[1]:
+        raise SomError(SOM_EDIM, f"{what} has {X.shape[1]} columns, the map has dim {d[1]}")
+    _need(X, n * d[1], what)
+
+
+def _hv(h) -> int:
+    return h.value if isinstance(h, ctypes.c_void_p) else int(h or 0)
 
 
 def _ptr(a, dtype=None, writable=False):
@@ -149,27 +186,52 @@ def som_schedule_default() -> som_schedule:
 def som_create(rows: int, cols: int, dim: int, topology: int, device: int = 0) -> ctypes.c_void_p:
     h = ctypes.c_void_p()
     _check(lib().som_create(rows, cols, dim, topology, device, ctypes.byref(h)))
+    _dims[_hv(h)] = (rows * cols, dim)
     return h
 
 
 def som_destroy(h) -> None:
+    _dims.pop(_hv(h), None)
     lib().som_destroy(h)
 
 
+def _check_map(h, w, what):
+    d = _dims.get(_hv(h))
+    if d is not None:
+        _need(w, d[0] * d[1], what)
+
+
 def som_set_weights(h, w) -> None:
+    _check_map(h, w, "w")
     _check(lib().som_set_weights(h, _ptr(w, np.float32)))
 
 
 def som_get_weights(h, w) -> None:
+    _check_map(h, w, "w")
     _check(lib().som_get_weights(h, _ptr(w, np.float32, writable=True)))
 
 
 def som_init_random(h, X, n: int, seed: int) -> None:
+    _check_rows(h, X, n)
     _check(lib().som_init_random(h, _ptr(X, np.float32), n, seed & (2**64 - 1)))
+
+
+def _check_log(bmu_log, t_begin, t_end, n, epochs):
+    if bmu_log is not None:
+        te = epochs * n if t_end == -1 else t_end
+        _need(bmu_log, max(te - t_begin, 0), "bmu_log")
+
+
+def _check_csr(rowptr, col, val, n):
+    _need(rowptr, n + 1, "rowptr")
+    if col is not None and val is not None and _numel(col) != _numel(val):
+        raise SomError(SOM_EDIM, "col and val differ in length")
 
 
 def som_train_online(h, X, n: int, epochs: int, alpha0: float, sigma0: float, sched: som_schedule | None,
                      seed: int, t_begin: int = 0, t_end: int = -1, bmu_log=None) -> None:
+    _check_rows(h, X, n)
+    _check_log(bmu_log, t_begin, t_end, n, epochs)
     sp = ctypes.byref(sched) if sched is not None else None
     _check(lib().som_train_online(h, _ptr(X, np.float32), n, epochs, alpha0, sigma0, sp, seed & (2**64 - 1),
                                   t_begin, t_end, _ptr(bmu_log, np.int32, writable=True)))
@@ -178,6 +240,8 @@ def som_train_online(h, X, n: int, epochs: int, alpha0: float, sigma0: float, sc
 def som_train_online_csr(h, rowptr, col, val, n: int, epochs: int, alpha0: float, sigma0: float,
                          sched: som_schedule | None, seed: int, t_begin: int = 0, t_end: int = -1,
                          bmu_log=None) -> None:
+    _check_csr(rowptr, col, val, n)
+    _check_log(bmu_log, t_begin, t_end, n, epochs)
     sp = ctypes.byref(sched) if sched is not None else None
     _check(lib().som_train_online_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                                       epochs, alpha0, sigma0, sp, seed & (2**64 - 1), t_begin, t_end,
@@ -185,12 +249,16 @@ def som_train_online_csr(h, rowptr, col, val, n: int, epochs: int, alpha0: float
 
 
 def som_train_batch(h, X, n: int, epochs: int, sigma0: float, sched: som_schedule | None = None, bmu=None) -> None:
+    _check_rows(h, X, n)
+    _need(bmu, n, "bmu")
     _check(lib().som_train_batch(h, _ptr(X, np.float32), n, epochs, sigma0,
                                  ctypes.byref(sched) if sched is not None else None, _ptr(bmu, np.int32, True)))
 
 
 def som_train_batch_csr(h, rowptr, col, val, n: int, epochs: int, sigma0: float, sched: som_schedule | None = None,
                         bmu=None) -> None:
+    _check_csr(rowptr, col, val, n)
+    _need(bmu, n, "bmu")
     _check(lib().som_train_batch_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                                      epochs, sigma0, ctypes.byref(sched) if sched is not None else None,
                                      _ptr(bmu, np.int32, True)))
@@ -225,11 +293,17 @@ def som_map_geometry(m: int, pc1: float, pc2: float) -> tuple[int, int, int]:
 
 
 def som_map(h, X, n: int, bmu1, bmu2=None, d2=None) -> None:
+    _check_rows(h, X, n)
+    for a, nm in ((bmu1, "bmu1"), (bmu2, "bmu2"), (d2, "d2")):
+        _need(a, n, nm)
     _check(lib().som_map(h, _ptr(X, np.float32), n, _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True),
                          _ptr(d2, np.float32, True)))
 
 
 def som_map_csr(h, rowptr, col, val, n: int, bmu1, bmu2=None, d2=None) -> None:
+    _check_csr(rowptr, col, val, n)
+    for a, nm in ((bmu1, "bmu1"), (bmu2, "bmu2"), (d2, "d2")):
+        _need(a, n, nm)
     _check(lib().som_map_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                              _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True), _ptr(d2, np.float32, True)))
 
@@ -263,24 +337,28 @@ def som_set_map_precision(h, precision: int) -> None:
 
 
 def som_qerror(h, X, n: int) -> float:
+    _check_rows(h, X, n)
     q = ctypes.c_double()
     _check(lib().som_qerror(h, _ptr(X, np.float32), n, ctypes.byref(q)))
     return q.value
 
 
 def som_topographic_error(h, X, n: int) -> float:
+    _check_rows(h, X, n)
     t = ctypes.c_double()
     _check(lib().som_topographic_error(h, _ptr(X, np.float32), n, ctypes.byref(t)))
     return t.value
 
 
 def som_errors(h, X, n: int) -> tuple[float, float]:
+    _check_rows(h, X, n)
     q, t = ctypes.c_double(), ctypes.c_double()
     _check(lib().som_errors(h, _ptr(X, np.float32), n, ctypes.byref(q), ctypes.byref(t)))
     return q.value, t.value
 
 
 def som_errors_csr(h, rowptr, col, val, n: int) -> tuple[float, float]:
+    _check_csr(rowptr, col, val, n)
     q, t = ctypes.c_double(), ctypes.c_double()
     _check(lib().som_errors_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
                                 ctypes.byref(q), ctypes.byref(t)))
@@ -288,6 +366,9 @@ def som_errors_csr(h, rowptr, col, val, n: int) -> tuple[float, float]:
 
 
 def som_umatrix(h, U) -> None:
+    d = _dims.get(_hv(h))
+    if d is not None:
+        _need(U, d[0], "U")
     _check(lib().som_umatrix(h, _ptr(U, np.float32, True)))
 
 
@@ -334,6 +415,23 @@ def som_comm_mailbox_ptr(h) -> int:
     v = ctypes.c_void_p()
     _check(lib().som_comm_mailbox_ptr(h, ctypes.byref(v)))
     return v.value or 0
+
+
+def som_comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().som_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def som_comm_init_nccl(h, rank: int, world: int, uid: bytes, shard_mode: int) -> None:
+    if len(uid) != 128:
+        raise SomError(SOM_EINVAL, "NCCL unique id must be 128 bytes")
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(lib().som_comm_init_nccl(h, rank, world, buf, shard_mode))
+
+
+def som_set_exchange(h, mode: int) -> None:
+    _check(lib().som_set_exchange(h, mode))
 
 
 def som_last_error() -> str:

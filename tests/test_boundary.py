@@ -73,3 +73,33 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "som_oracle" not in txt, f
+
+
+def test_binding_rejects_mismatched_shapes():
+    """the binding checks array sizes against the handle before
+    any C call (SOM_EDIM) — a fake handle registered with its
+    map shape is enough, nothing reaches the library."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_1905_09598_b200 import som
+    h = ctypes.c_void_p(0x1234)
+    som._dims[0x1234] = (4, 3)
+    try:
+        bad = [lambda: som.som_map(h, np.zeros((2, 5), np.float32), 2, np.zeros(2, np.int32)),
+               lambda: som.som_map(h, np.zeros((2, 3), np.float32), 3, np.zeros(3, np.int32)),
+               lambda: som.som_map(h, np.zeros((2, 3), np.float32), 2, np.zeros(1, np.int32)),
+               lambda: som.som_get_weights(h, np.zeros((3, 3), np.float32)),
+               lambda: som.som_set_weights(h, np.zeros(11, np.float32)),
+               lambda: som.som_train_online(h, np.zeros((5, 4), np.float32), 5, 1, 0.1, 1.0, None, 1),
+               lambda: som.som_train_online(h, np.zeros((5, 3), np.float32), 5, 2, 0.1, 1.0, None, 1, 0, -1,
+                                            np.zeros(9, np.int32)),
+               lambda: som.som_umatrix(h, np.zeros(3, np.float32)),
+               lambda: som.som_errors_csr(h, np.zeros(2, np.int64), np.zeros(1, np.int32), np.zeros(1, np.float32), 2)]
+        for f in bad:
+            with pytest.raises(som.SomError) as e:
+                f()
+            assert e.value.status == som.SOM_EDIM
+    finally:
+        som._dims.pop(0x1234, None)

@@ -460,3 +460,97 @@ def test_map_geometry_fig2_traces():
     assert oracle.map_geometry(4, 1.0, 1.0) == (3, 3, 1808)
     r, c, _ = oracle.map_geometry(100, 10.0, 0.05)       # pc2 * munits < pc1 -> r = 1
     assert (r, c) == oracle.map_geometry(100, 1.0, 1.0)[:2] == (6, 8)
+
+
+# ------------------------------------------- round 2: discriminating pins
+@pytest.mark.parametrize("topo,key", [(0, "rect"), (1, "hex")])
+def test_topographic_error_nonzero_closed_form(topo, key):
+    """A non-zero TE fixed by hand (tests/golden/te_2x2_docs.json): the BMU
+    pairs, which pairs are lattice-adjacent, TE = k/n exactly, and the zero
+    row left out of both QE and TE."""
+    g = _gold("te_2x2_docs.json")
+    W = np.array(g["W"], np.float32)
+    X = np.array(g["docs"], np.float32)
+    b1, b2, d1 = oracle.map_docs(W, X)
+    assert [[int(a), int(b)] for a, b in zip(b1, b2)] == g["bmu_pairs"]
+    np.testing.assert_allclose(d1, [min(r) for r in g["D_hand"]], rtol=1e-6, atol=1e-7)
+    nonadj = {tuple(sorted(p)) for p in g[key]["nonadjacent_pairs"]}
+    for u in range(4):
+        for v in range(u + 1, 4):
+            assert (oracle.lattice_g2(2, 2, topo, u, v) != 1.0) == ((u, v) in nonadj)
+    keep = oracle.keep_mask(len(X), oracle.nonzero_rows(X))
+    assert keep.tolist() == g["keep"]
+    k, n = g[key]["te"]
+    assert oracle.topographic_error_from_bmus(2, 2, topo, b1, b2, keep) == k / n
+    assert oracle.topographic_error(W, 2, 2, topo, X) == k / n
+    k2, n2 = g[key]["te_if_zero_row_counted"]
+    assert oracle.topographic_error_from_bmus(2, 2, topo, b1, b2) == k2 / n2
+    qe = (0.4 + 1.0 + 0.3 + 2 * math.sqrt(6.85) + math.sqrt(12.5)) / 6
+    assert abs(oracle.qerror(W, X) - qe) < 1e-6
+
+
+def test_decay_kinds_mid_schedule_closed_forms():
+    """The three decay forms of R1 at tau = 1/2 and 1/4 with k = ln 100:
+    Gaussian f = 100^(-tau^2), linear f = 1 - 0.99 tau, exponential
+    f = 100^(-tau) — alpha_t = alpha0 f and sigma_t = sigma0 f (above the
+    floor).  A squared tau in the linear or exponential kind, or a missing
+    square in the Gaussian one, fails here."""
+    T = 1000
+    want = {0: {500: 10 ** -0.5, 250: 100 ** (-1 / 16)},
+            1: {500: 0.505, 250: 1 - 0.99 / 4},
+            2: {500: 0.1, 250: 100 ** -0.25}}
+    for kind, pts in want.items():
+        for t, f in pts.items():
+            a, s, r2 = oracle.schedule(t, T, 1.0, 40.0, kind=kind)
+            assert math.isclose(a, f, rel_tol=1e-14), (kind, t, a, f)
+            assert math.isclose(s, 40.0 * f, rel_tol=1e-14)
+            assert math.isclose(r2, 2 * (40.0 * f) ** 2 * math.log(1e4), rel_tol=1e-13)
+
+
+def test_zero_rows_never_drawn_and_not_scored():
+    """all-zero rows stay in X but are excluded from the draws:
+    draw t takes the i_t-th non-zero row, i_t = sample_index(seed, t, n_nz).
+    So X with zero rows inserted trains exactly like the zero-free X when T
+    is the same (epochs * n = epochs' * n_nz) — and a corpus of zero rows
+    only is EmptyData (S:219)."""
+    C = bank_corpus(40, 60, seed=9)
+    Xnz = C.dense()
+    X = np.zeros((60, 60), np.float32)
+    pos = np.sort(np.random.default_rng(1).choice(60, 40, replace=False))
+    X[pos] = Xnz
+    assert np.array_equal(oracle.nonzero_rows(X), pos)
+    W0 = init_rows(Xnz, 9, 2)
+    # T = 2 * 60 = 3 * 40 = 120 steps on both
+    Wa, la = oracle.train_online(W0, 3, 3, 1, X, epochs=2, alpha0=0.1, sigma0=1.5, seed=7)
+    Wb, lb = oracle.train_online(W0, 3, 3, 1, Xnz, epochs=3, alpha0=0.1, sigma0=1.5, seed=7)
+    assert np.array_equal(Wa, Wb) and np.array_equal(la, lb)
+    assert oracle.qerror(Wa, X) == oracle.qerror(Wa, Xnz)
+    assert oracle.topographic_error(Wa, 3, 3, 1, X) == oracle.topographic_error(Wa, 3, 3, 1, Xnz)
+    with pytest.raises(ValueError, match="EmptyData"):
+        oracle.train_online(W0, 3, 3, 1, np.zeros((5, 60), np.float32), epochs=1, alpha0=0.1, sigma0=1.5, seed=7)
+    # CSR: explicit zeros do not make a row non-zero
+    rp = np.array([0, 2, 3, 3], np.int64)
+    va = np.array([0.5, 0.0, 0.0], np.float32)
+    assert oracle.nonzero_rows_csr(rp, va).tolist() == [0]
+
+
+def test_csr_training_equals_dense_training():
+    """or_train_online_csr densifies x_t per step: the same trajectory as the
+    dense oracle on the dense copy, including a corpus with zero rows (an
+    explicit-zero CSR entry does not make a row non-zero)."""
+    C = bank_corpus(80, 120, seed=12)
+    W0 = init_rows(C.dense(), 16, 3)
+    Wa, la = oracle.train_online(W0, 4, 4, 1, C.dense(), epochs=3, alpha0=0.2, sigma0=2.0, seed=5)
+    Wb, lb = oracle.train_online_csr(W0, 4, 4, 1, C.indptr, C.indices, C.data, epochs=3, alpha0=0.2, sigma0=2.0,
+                                     seed=5)
+    assert np.array_equal(Wa, Wb) and np.array_equal(la, lb)
+    # zero rows: rows 3 and 7 emptied (row 7 keeps an explicit 0.0 entry)
+    rp, ci, va = C.indptr.copy(), C.indices.copy(), C.data.copy()
+    va[rp[3]:rp[4]] = 0.0
+    va[rp[7]:rp[8]] = 0.0
+    X = C.dense()
+    X[3] = 0.0
+    X[7] = 0.0
+    Wa, la = oracle.train_online(W0, 4, 4, 1, X, epochs=2, alpha0=0.2, sigma0=2.0, seed=6)
+    Wb, lb = oracle.train_online_csr(W0, 4, 4, 1, rp, ci, va, epochs=2, alpha0=0.2, sigma0=2.0, seed=6)
+    assert np.array_equal(Wa, Wb) and np.array_equal(la, lb)
