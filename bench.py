@@ -1,15 +1,25 @@
 #!/usr/bin/env python
 """bench.py — the CUDASOM hot path on B200, one JSON line on rank 0.
 
-A "step" is one pass of the whole hot path over
-one synthetic c2 workload (BASELINE.json configs[1]): 20x20 hex map,
-5,000 x 3,000 L2-normalised TF-IDF corpus, 100 epochs of online training
-(T = 500,000 samples) from a seeded row init, then batch mapping of all
-documents, QE + TE, and the U-matrix.  value = training samples/s over the
-whole step, summed over ranks (each rank runs its own independent problem:
-weak scaling, no data-path collective).
+Headline (BASELINE.json configs[2], the largest config one GPU holds; c4 and
+c5 are the sharded configs, configs[0]/[1] are parity cases): a "step" is one
+pass of the whole hot path over the c3 workload:
+50x50 hex map, 50,000 x 10,000 L2-normalised TF-IDF corpus (CSR, the DTM of
+P:148-154), seeded row init + 10 epochs of online training (T = 500,000
+samples) + batch mapping of all 50,000 documents + QE/TE + U-matrix, all in
+one libsom call (som_fit_csr).  value = training samples/s of the whole step.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+At N > 1 the same job is split: training neuron-sharded (units u = r + N l,
+in-kernel NVLink winner exchange), the trained map gathered once, mapping
+and errors document-sharded (errors reduced over libsom's NCCL
+communicator) — strong scaling of one job.
+
+Secondary keys: the full c5 mapping job (10M CSR documents onto 100x100,
+document-sharded), c4 training (neuron-sharded at N > 1; mailbox vs NCCL
+exchange latency), the c2 step of round 1, the paper's Table 3 study, batch
+SOM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
   python bench.py --impl reference ...   # the oracle (CPU) on a bounded sample
 """
 from __future__ import annotations
@@ -32,6 +42,10 @@ from synth import CONFIGS, bank_corpus  # noqa: E402
 
 METRIC = "SOM training samples/sec and batch BMU-mapping docs/sec at 1/2/4/8 B200"
 ALPHA0 = 0.1
+PAPER_44X = ("CUDASOM's average speed-up of 44x over its CPU SOM (PAPER.md:35; 41-47x per run, Table 2 PAPER.md:286-296) "
+             "on an NVIDIA Quadro P5000 (Pascal, CUDA 8.0, PyCUDA) vs an Intel Xeon E5-2640 v4 @ 2.4 GHz (PAPER.md:223-225)"
+             ": context only, other hardware and a different CPU baseline")
+C5_DOCS, C5_BLOCK = 10_000_000, 200_000
 
 
 def parse():
@@ -40,16 +54,15 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3"])
     p.add_argument("--epochs", type=int, default=None, help="override epochs (diagnostics only)")
-    p.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline legs")
     p.add_argument("--seed", type=int, default=1)
-    p.add_argument("--map-docs", type=int, default=200000, help="documents in the c5-shaped mapping leg (0 = skip)")
-    p.add_argument("--c3-steps", type=int, default=20000, help="steps of the c3 training leg (0 = skip)")
+    p.add_argument("--c5-docs", type=int, default=C5_DOCS, help="documents of the c5 mapping job (0 = skip)")
+    p.add_argument("--c4-steps", type=int, default=2000, help="steps of the c4 training leg (0 = skip)")
+    p.add_argument("--c2-steps", type=int, default=1, help="timed c2 steps of the round-1 leg (0 = skip)")
     p.add_argument("--table3-steps", type=int, default=20000, help="steps per map of the Table 3 leg (0 = skip)")
     p.add_argument("--batch-epochs", type=int, default=10, help="epochs of the batch-SOM leg (0 = skip)")
-    p.add_argument("--c4-steps", type=int, default=2000, help="steps of the c4 (neuron-sharded at N > 1) leg (0 = skip)")
-    p.add_argument("--c4-docs", type=int, default=20000, help="documents of the c4 leg (replicated on every rank)")
     return p.parse_args()
 
 
@@ -111,161 +124,76 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def workload(cfg_name, seed, epochs_override):
-    cfg = dict(CONFIGS[cfg_name])
-    if epochs_override is not None:
-        cfg["epochs"] = epochs_override
-    C = bank_corpus(cfg["n"], cfg["d"], seed=seed)
-    return cfg, C
+# ------------------------------------------------------------------ peaks
+def _json(path):
+    with open(os.path.join(ROOT, path)) as f:
+        return json.load(f)
+
+
+def hbm_peak_gbs():
+    try:
+        return float(_json("MEASURED_PEAKS.json")["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except Exception:
+        return 6550.0, "fallback 6.55 TB/s (B200_PROFILING.md)"
+
+
+def l2_peak_gbs(footprint_mb=96):
+    """Measured L2 read+write bandwidth at a footprint just below the L2
+    (profiles/probes_r01.json, tools/probes.cu)."""
+    try:
+        j = _json("profiles/probes_r01.json")["l2_rw_GBps"]
+        return float(j[str(footprint_mb)]), f"measured L2 read+write bandwidth at a {footprint_mb} MB footprint " \
+                                            "(profiles/probes_r01.json l2_rw_GBps)"
+    except Exception:
+        return 12144.0, "fallback 12.1 TB/s L2 read+write (profiles/probes_r01.json missing)"
 
 
 def train_peak_tflops():
-    """Peak of the training kernel's exact distance element (1 F2F.F64.F32 +
-    DADD + DFMA = 3 flop): bound by the measured fp32->fp64 conversion rate
-    (profiles/probe_fp64.json) x 148 SMs x max SM clock."""
-    path = os.path.join(ROOT, "profiles", "probe_fp64.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            j = json.load(f)
+    """Peak of the exact distance element (1 F2F.F64.F32 + DADD + DFMA = 3
+    flop): the measured fp32->fp64 conversion rate x 148 SMs x max clock."""
+    try:
+        j = _json("profiles/probe_fp64.json")
         return 3.0 * j["train_element_peak_per_s"] / 1e12, ("measured F2F.F64.F32 rate "
                                                             f"{j['f2f_per_clk_per_sm']}/clk/SM x 148 SMs x 1965 MHz "
                                                             "x 3 flop/element (profiles/probe_fp64.json)")
-    return 3.0 * 16 * 148 * 1965e6 / 1e12, "nominal 16 F2F/clk/SM x 148 x 1965 MHz x 3 flop (no measurement file)"
+    except Exception:
+        return 3.0 * 16 * 148 * 1965e6 / 1e12, "nominal 16 F2F/clk/SM x 148 x 1965 MHz x 3 flop (no measurement file)"
 
 
 def tf32_peak_tflops():
     """Dense TF32 peak: the measured bf16 cuBLAS peak (MEASURED_PEAKS.json,
     burst) x the nominal tf32/bf16 ratio 1.1/2.25 (B200_PROFILING.md)."""
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            bf16 = float(json.load(f)["bf16_tflops"])
+    try:
+        bf16 = float(_json("MEASURED_PEAKS.json")["bf16_tflops"])
         return bf16 * 1.1 / 2.25, f"measured bf16 {bf16} TFLOP/s x 1.1/2.25 (MEASURED_PEAKS.json)"
-    return 1590.0 * 1.1 / 2.25, "fallback bf16 1590 TFLOP/s x 1.1/2.25 (B200_PROFILING.md)"
+    except Exception:
+        return 1590.0 * 1.1 / 2.25, "fallback bf16 1590 TFLOP/s x 1.1/2.25 (B200_PROFILING.md)"
 
 
 def conv_peak_per_s():
-    """fp32 -> fp64 conversions per second (F2F.F64.F32, the bound of the
-    fp32-stored sparse mapping kernel and of the training distance): the
-    measured per-SM rate (profiles/probe_fp64.json) x 148 SMs x max clock."""
-    path = os.path.join(ROOT, "profiles", "probe_fp64.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            j = json.load(f)
+    """fp32 -> fp64 conversions per second (F2F.F64.F32): the measured per-SM
+    rate (profiles/probe_fp64.json) x 148 SMs x max clock."""
+    try:
+        j = _json("profiles/probe_fp64.json")
         return j["train_element_peak_per_s"], (f"measured F2F.F64.F32 rate {j['f2f_per_clk_per_sm']}/clk/SM x 148 "
                                                "SMs x 1965 MHz (profiles/probe_fp64.json)")
-    return 16 * 148 * 1965e6, "nominal 16 F2F/clk/SM x 148 x 1965 MHz (no measurement file)"
+    except Exception:
+        return 16 * 148 * 1965e6, "nominal 16 F2F/clk/SM x 148 x 1965 MHz (no measurement file)"
 
 
-def mapping_leg(som, torch, args, local, seed, world=1, rank=0):
-    """Batch BMU mapping docs/s on a c5-shaped sample (BASELINE.json configs[4]:
-    100x100 map, 20k terms, CSR documents; the full 10M-document job is the
-    doc-sharded multi-GPU case) through som_map_csr.  Main: the default (AUTO)
-    path, the exact fp64 sparse identity (map_sparse.cu, R25); beside it the
-    dense tcgen05 3xTF32 contraction (map_tc.cu) on the same documents, and
-    the oracle's sparse-identity mapping on the host cores for a sample."""
-    cfg = CONFIGS["c5"]
-    n, d, N = args.map_docs, cfg["d"], cfg["rows"] * cfg["cols"]
-    C = bank_corpus(n, d, seed=seed + 500)
-    Wsrc = bank_corpus(N, d, seed=args.seed + 501).dense()     # the map is replicated on every rank
-    W = (0.5 * Wsrc + 0.5 / np.sqrt(d)).astype(np.float32)
-    del Wsrc
-    mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
-    som.som_set_stream(mm.h, torch.cuda.current_stream())
-    mm.set_weights(torch.from_numpy(W).cuda())
-    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
-    b1 = torch.empty(n, dtype=torch.int32, device="cuda")
-    b2 = torch.empty(n, dtype=torch.int32, device="cuda")
-    d1 = torch.empty(n, dtype=torch.float32, device="cuda")
-
-    def timed(precision):
-        som.som_set_map_precision(mm.h, precision)
-        som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)          # warm-up (W^T / W split, scratch)
-        times, kern = [], []
-        for _ in range(max(3, args.steps)):
-            torch.cuda.synchronize()
-            som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)
-            ms, _, launches = som.som_last_stats(mm.h)
-            times.append(ms)
-            kern.append(launches)
-        return statistics.mean(times), kern[-1]
-
-    ms, launches = timed(som.SOM_MAP_AUTO)
-    sp_b1 = b1.cpu().numpy()
-    # end to end through the C ABI with pinned HOST buffers: the CSR arrays
-    # go host -> device and bmu1, bmu2, D1 come back inside the timed call
-    hrp, hci, hva = (torch.from_numpy(a).pin_memory() for a in (C.indptr, C.indices, C.data))
-    hb1 = torch.empty(n, dtype=torch.int32).pin_memory()
-    hb2 = torch.empty(n, dtype=torch.int32).pin_memory()
-    hd1 = torch.empty(n, dtype=torch.float32).pin_memory()
-    som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)     # warm-up (staging buffers)
-    e2e = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)
-        e2e.append(time.perf_counter() - t0)
-    e2e_s = statistics.mean(e2e)
-    h2d_map = hrp.numel() * 8 + hci.numel() * 4 + hva.numel() * 4
-    d2h_map = n * 12
-    # document sharding (SURVEY §8.E): every rank maps its own n documents;
-    # the job time is the slowest rank's, the error sums are all-reduced
-    qe_l, te_l = som.som_errors_csr(mm.h, rp, ci, va, n)
-    err_ms, _, _ = som.som_last_stats(mm.h)
-    ms_max, qe, te = ms, qe_l, te_l
-    if world > 1:
-        import torch.distributed as dist
-        from paper_1905_09598_b200 import dist as sdist
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-        qe, te = sdist.reduce_errors(qe_l, te_l, n, device=torch.device("cuda", local))
-    ms_tc, launches_tc = timed(som.SOM_MAP_3XTF32)
-    agree = float(np.mean(b1.cpu().numpy() == sp_b1))
-    mm.close()
-    fma = float(C.nnz) * N
-    cpk, cpk_src = conv_peak_per_s()
-    icv_peak = 2.0 * min(cpk / (148 * 1965e6), 12.8) * 148 * 1965e6
-    flop = 2.0 * n * N * d
-    peak, src = tf32_peak_tflops()
-    executed = 3.0 * flop / (ms_tc / 1000.0) / 1e12
-
-    cpu = None
-    if not args.no_baseline and rank == 0:
-        import oracle
-        ns = min(n, 40000)                                   # ~10 s on 16 host cores
-        t0 = time.perf_counter()
-        oracle.map_docs_csr(W, C.indptr[:ns + 1], C.indices[:C.indptr[ns]], C.data[:C.indptr[ns]])
-        dt = time.perf_counter() - t0
-        cpu = {"value": ns / dt, "unit": "docs/s", "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": f"first {ns} documents, fp64 sparse-identity oracle (or_map_csr, OpenMP over docs), "
-                         f"{dt:.1f} s"}
-    return {"workload": f"c5-shaped sample: {n} CSR docs ({C.nnz / n:.1f} nnz/doc) x {N} units x {d} terms "
-                        f"per GPU, document-sharded over {world} GPU(s)",
-            "docs_per_s": world * n / (ms_max / 1000.0), "ms": ms_max, "launches": launches, "n_gpus": world,
-            "e2e": {"docs_per_s_rank0": n / e2e_s, "h2d_bytes": h2d_map, "d2h_bytes": d2h_map,
-                    "what": "som_map_csr with pinned host CSR arrays and host outputs, wall clock per call"},
-            "scaling": "weak", "qe": qe, "te": te, "errors_ms_rank0": err_ms,
-            "path": "exact fp64 sparse identity (SOM_MAP_SPARSE_F64, AUTO)",
-            "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T, integer widening> (rank 0)",
-                         "achieved": fma / (ms / 1000.0) / 1e12, "peak": icv_peak / 1e12, "unit": "T conv+FMA/s",
-                         "frac": fma / (ms / 1000.0) / icv_peak,
-                         "peak_source": "fp32->fp64 widening split 50/50 between the F2F pipe (" + cpk_src + ") and "
-                                        "the integer pipe (5 ALU ops per value on 64 lanes/clk/SM = 12.8/clk/SM, "
-                                        "B300_MICROARCH pipe rates): 2 x min(15.43, 12.8)/clk/SM x 148 x 1965 MHz; "
-                                        "the map is non-negative, so the kernel widens half the values on the "
-                                        "integer pipe",
-                         "work": "nnz*N fp32->fp64 conversions + fp64 FMAs per call (one per non-zero per unit), "
-                                 "incl. the top-2 merge kernel"},
-            "cpu_baseline": cpu,
-            "tc_3xtf32": {"docs_per_s": n / (ms_tc / 1000.0), "ms": ms_tc, "launches": launches_tc,
-                          "bmu1_agreement_with_exact": agree,
-                          "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
-                                       "achieved": executed, "peak": peak, "unit": "TFLOP/s",
-                                       "frac": executed / peak, "peak_source": src,
-                                       "work": "3 x 2*n*N*d executed TF32 flop per call (3xTF32 split), incl. "
-                                               "CSR split + merge",
-                                       "algorithmic_fp32_tflops": flop / (ms_tc / 1000.0) / 1e12}}}
+def icv_peak_per_s():
+    """Split-widening peak of the sparse mapping kernel: half the values on
+    the F2F pipe, half widened exactly on the integer pipe (5 ALU ops); the
+    integer rate is the measured one when profiles/probe_icv.json exists."""
+    cpk, src = conv_peak_per_s()
+    f2f_clk = cpk / (148 * 1965e6)
+    try:
+        j = _json("profiles/probe_icv.json")
+        icv_clk, isrc = float(j["icv_per_clk_per_sm"]), "measured integer widening rate (profiles/probe_icv.json)"
+    except Exception:
+        icv_clk, isrc = 12.8, "nominal 64 INT lanes/clk/SM / 5 ops (B300_MICROARCH pipe rates)"
+    return 2.0 * min(f2f_clk, icv_clk) * 148 * 1965e6, f"2 x min(F2F {f2f_clk:.2f}, ICV {icv_clk:.2f})/clk/SM x 148 " \
+                                                         f"x 1965 MHz; F2F: {src}; ICV: {isrc}"
 
 
 def updated_units(rows, cols, topo, bmu_log, t0, T, sigma0, eps=1e-4, k=math.log(100.0), sigma_min=1.0):
@@ -288,153 +216,300 @@ def updated_units(rows, cols, topo, bmu_log, t0, T, sigma0, eps=1e-4, k=math.log
     return out
 
 
-def batch_leg(som, torch, args, local, seed):
-    """Batch SOM (R27, som_train_batch_csr) on the c3 shape: 50x50 hex map,
-    50,000 CSR documents x 10,000 terms, `--batch-epochs` epochs; every epoch
-    maps all documents (exact sparse path), buckets them by BMU, sums them
-    per unit in fp64 and applies the lattice kernel (N x N x (d+1) fp64
-    contraction)."""
-    cfg = CONFIGS["c3"]
-    C = bank_corpus(cfg["n"], cfg["d"], seed=seed + 300)
-    N = cfg["rows"] * cfg["cols"]
-    from synth import init_rows
-    W0 = torch.from_numpy(init_rows(C.dense()[:5000], N, seed + 301)).cuda(local)
-    rp, ci, va = (torch.from_numpy(a).cuda(local) for a in (C.indptr, C.indices, C.data))
-    E = args.batch_epochs
-    with som.SOM(cfg["rows"], cfg["cols"], cfg["d"], cfg["topo"], device=local) as m:
-        som.som_set_stream(m.h, torch.cuda.current_stream())
-        m.set_weights(W0)
-        som.som_train_batch_csr(m.h, rp, ci, va, C.n, 1, cfg["sigma0"], None, None)     # warm-up
-        m.set_weights(W0)
-        som.som_train_batch_csr(m.h, rp, ci, va, C.n, E, cfg["sigma0"], None, None)
-        ms, units, launches = som.som_last_stats(m.h)
-    gemm_fma = float(N) * N * (cfg["d"] + 1) * E
-    return {"workload": f"c3 shape: {cfg['rows']}x{cfg['cols']} hex, {C.n} CSR docs x {cfg['d']} terms, {E} epochs",
-            "docs_per_s": units / (ms / 1e3), "ms_per_epoch": ms / E, "launches": launches,
-            "upper_bound_gemm_tflops": 2.0 * gemm_fma / (ms / 1e3) / 1e12,
-            "note": "upper_bound_gemm_tflops counts the full N x N x (d+1) fp64 contraction per epoch over the "
-                    "whole epoch time (mapping, bucketing, sums included); tiles outside the cutoff are skipped"}
+def train_bytes(N, d, nnz_x, H, sparse):
+    """Algorithmic bytes of one training step:
+    dense rows: read W (4 N d) + write the H_t updated rows (4 H_t d) + x_t;
+    sparse rows (R25, the kernel family that runs on TF-IDF rows): read and
+    write the H_t updated rows (8 H_t d) + one fp32 gathered per non-zero of
+    x_t for every other unit (4 nnz (N - H_t)) + x_t's CSR entries."""
+    H = np.asarray(H, np.float64)
+    if sparse:
+        return float(np.sum(8.0 * H * d + 4.0 * nnz_x * (N - H) + 8.0 * nnz_x))
+    return float(np.sum(4.0 * N * d + 4.0 * H * d + 4.0 * d))
 
 
-def exchange_probe(som, torch, args, local, rank, world):
-    """Per-step cost of the winner exchange alone: a map of 16 units per GPU
-    with d = 64 (negligible work per step), 20,000 steps; at N > 1 neuron-
-    sharded (in-GPU all-gather + cross-GPU mailbox exchange over NVLink),
-    at N = 1 the in-GPU all-gather only.  The difference is the cross-GPU
-    latency the sharded training pays every step."""
+def config_dict(name, cfg, world):
+    """The config both arms report (identical keys and values)."""
+    return {"workload": name, "map": f"{cfg['rows']}x{cfg['cols']} {'hex' if cfg['topo'] else 'rect'}",
+            "docs": cfg["n"], "terms": cfg["d"], "epochs": cfg["epochs"], "samples_per_step": cfg["epochs"] * cfg["n"],
+            "alpha0": ALPHA0, "sigma0": cfg["sigma0"], "cutoff": 1e-4, "input": "CSR (TF-IDF DTM)",
+            "step": "init + full online training + mapping of all docs + QE/TE + U-matrix (som_fit_csr)",
+            "parallelism": "1 GPU" if world == 1 else f"neuron-sharded training + document-sharded mapping over "
+                                                      f"{world} GPUs",
+            "l2": "flushed between timed steps (256 MB write)"}
+
+
+# ------------------------------------------------------------- c5 corpus
+def _c5_block(k):
+    C = bank_corpus(C5_BLOCK, CONFIGS["c5"]["d"], seed=9000 + k)
+    return C.indptr, C.indices, C.data
+
+
+def c5_corpus(n_docs, rank, world):
+    """This rank's contiguous share of the c5 corpus (BASELINE configs[4]):
+    blocks of 200,000 documents generated by seed (the same corpus as
+    tests/test_gpu_full_size.py), built in parallel host processes."""
+    import multiprocessing as mp
+    nb = max(1, n_docs // C5_BLOCK)
+    from paper_1905_09598_b200.dist import shard_range
+    lo, hi = shard_range(nb, rank, world)
+    ks = list(range(lo, hi))
+    if not ks:
+        return np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), 0
+    with mp.get_context("fork").Pool(min(16, max(1, (os.cpu_count() or 2) // max(1, world)))) as pool:
+        parts = pool.map(_c5_block, ks)
+    nnz = sum(p[1].size for p in parts)
+    n = sum(p[0].size - 1 for p in parts)
+    rowptr = np.empty(n + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    rowptr[0] = 0
+    r = o = 0
+    for ip, ci, va in parts:
+        m = ip.size - 1
+        rowptr[r + 1:r + m + 1] = ip[1:] + o
+        col[o:o + ci.size] = ci
+        val[o:o + va.size] = va
+        r += m
+        o += ci.size
+    return rowptr, col, val, n
+
+
+def c5_codebook():
+    d = CONFIGS["c5"]["d"]
+    return (0.5 * bank_corpus(10000, d, seed=8999).dense() + 0.5 / np.sqrt(d)).astype(np.float32)
+
+
+# ------------------------------------------------------------- B200 legs
+def c5_leg(som, torch, args, local, rank, world, corpus):
+    """BASELINE.json configs[4]: batch BMU mapping of 10,000,000 CSR
+    documents x 20,000 terms onto a 100x100 hex map, document-sharded over
+    the ranks (each maps its contiguous share; QE/TE reduced over libsom's
+    NCCL communicator).  docs/s = all documents / slowest rank's device time.
+    Default path: the exact fp64 sparse identity (R25, map_sparse.cu)."""
     import torch.distributed as dist
-    from synth import uniform_matrix
-    side_c = 16
-    steps, n = 20000, 2000
-    X = torch.from_numpy(uniform_matrix(n, 64, args.seed + 700)).cuda(local)
-    W0 = torch.from_numpy(uniform_matrix(world * side_c, 64, args.seed + 701)).cuda(local)
-    ok = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ms = 0.0
-    sm = None
-    try:
-        if world > 1:
-            from paper_1905_09598_b200.dist import ShardedSOM
-            sm = ShardedSOM(world, side_c, 64, 1, rank, world, device=local)
-            sm.set_weights(W0)
-    except Exception:
-        ok[0] = 1.0
+    rowptr, col, val, n = corpus
+    cfg = CONFIGS["c5"]
+    N, d = cfg["rows"] * cfg["cols"], cfg["d"]
+    W = torch.from_numpy(c5_codebook()).cuda(local)
+    mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+    som.som_set_stream(mm.h, torch.cuda.current_stream())
     if world > 1:
-        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
-        if ok.item() > 0:
-            return {"error": "set-up failed"}
-    try:
-        if world > 1:
-            dist.barrier()
-            som.som_train_online(sm.h, X, n, 10, ALPHA0, 8.0, None, args.seed, 0, steps, None)
-            ms, _, _ = som.som_last_stats(sm.h)
-            sm.close()
-        else:
-            with som.SOM(1, side_c, 64, 1, device=local) as m1:
-                m1.set_weights(W0)
-                som.som_train_online(m1.h, X, n, 10, ALPHA0, 8.0, None, args.seed, 0, steps, None)
-                ms, _, _ = som.som_last_stats(m1.h)
-    except Exception:
-        ok[0] = 1.0
-    if world > 1:
-        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
-    if ok.item() > 0:
-        return {"error": "exchange probe failed"}
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        from paper_1905_09598_b200 import dist as sdist
+        sdist.init_nccl(mm.h, rank, world, som.SOM_SHARD_DOCS)
+    mm.set_weights(W)
+    rp, ci, va = (torch.from_numpy(a).cuda(local) for a in (rowptr, col, val))
+    b1 = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    b2 = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    d1 = torch.empty(max(n, 1), dtype=torch.float32, device="cuda")
+    som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)            # warm-up (W^T, scratch)
+    times, launches = [], 0
+    for _ in range(max(3, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        som.som_map_csr(mm.h, rp, ci, va, n, b1, b2, d1)
+        ms, _, launches = som.som_last_stats(mm.h)
+        times.append(ms)
+    ms = statistics.mean(times)
+    qe, te = som.som_errors_csr(mm.h, rp, ci, va, n)            # collective at N > 1
+    err_ms = som.som_last_stats(mm.h)[0]
+    t = torch.tensor([ms, err_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"us_per_step": 1000.0 * float(t[0]) / steps, "units_per_gpu": side_c, "d": 64, "steps": steps,
-            "what": ("in-GPU all-gather + cross-GPU mailbox exchange" if world > 1 else "in-GPU all-gather only")}
+    ms_max, err_max = float(t[0]), float(t[1])
+    # end to end: pinned host CSR arrays in, host outputs back, wall clock
+    hrp, hci, hva = (torch.from_numpy(a).pin_memory() for a in (rowptr, col, val))
+    hb1, hb2 = (torch.empty(max(n, 1), dtype=torch.int32).pin_memory() for _ in range(2))
+    hd1 = torch.empty(max(n, 1), dtype=torch.float32).pin_memory()
+    som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)       # warm-up (staging buffers)
+    e2e = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        som.som_map_csr(mm.h, hrp, hci, hva, n, hb1, hb2, hd1)
+        e2e.append(time.perf_counter() - t0)
+    te2e = torch.tensor([statistics.mean(e2e)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te2e, op=dist.ReduceOp.MAX)
+    # beside it: the tcgen05 3xTF32 contraction on a 200k-document sample
+    ns = min(n, 200_000)
+    som.som_set_map_precision(mm.h, som.SOM_MAP_3XTF32)
+    som.som_map_csr(mm.h, rp, ci, va, ns, b1, b2, d1)
+    tc_ms = []
+    for _ in range(2):
+        som.som_map_csr(mm.h, rp, ci, va, ns, b1, b2, d1)
+        tc_ms.append(som.som_last_stats(mm.h)[0])
+    tcm = statistics.mean(tc_ms)
+    mm.close()
+    nnz = float(val.size)
+    work = nnz * N                                               # conversions + FMAs (one per non-zero per unit)
+    peak, psrc = icv_peak_per_s()
+    tpeak, tsrc = tf32_peak_tflops()
+    executed = 3.0 * 2.0 * ns * N * d / (tcm / 1e3) / 1e12
+    cpu = None
+    if rank == 0 and not args.no_baseline:
+        import oracle
+        nsb = min(n, 40000)                                        # ~10 s on 16 host cores
+        t0 = time.perf_counter()
+        oracle.map_docs_csr(c5_codebook(), rowptr[:nsb + 1], col[:rowptr[nsb]], val[:rowptr[nsb]])
+        dt = time.perf_counter() - t0
+        cpu = {"value": nsb / dt, "unit": "docs/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": f"first {nsb} documents of the c5 corpus, fp64 sparse-identity oracle (or_map_csr, "
+                         f"OpenMP over documents), {dt:.1f} s"}
+    n_all = n * world if world > 1 else n
+    total = args.c5_docs if world > 1 else n
+    return {"workload": f"c5: {total} CSR docs ({nnz / max(n, 1):.1f} nnz/doc) x 100x100 hex x {d} terms, "
+                        f"{'document-sharded over ' + str(world) + ' GPUs' if world > 1 else '1 GPU'}",
+            "docs_per_s": total / (ms_max / 1e3), "ms": ms_max, "launches_rank0": launches,
+            "scaling": "strong (fixed 10M-document job)" if world > 1 else None, "n_gpus": world,
+            "qe": qe, "te": te, "errors_ms": err_max, "docs_rank0": n, "docs_all": n_all,
+            "e2e": {"docs_per_s": total / float(te2e[0]), "h2d_bytes_rank0": int(rowptr.nbytes + col.nbytes + val.nbytes),
+                    "d2h_bytes_rank0": 12 * n, "what": "som_map_csr with pinned host CSR arrays and host outputs "
+                                                        "(max over ranks, wall clock)"},
+            "path": "exact fp64 sparse identity (R25; AUTO)",
+            "roofline": {"bound": "alu", "kernel": "map_sparse_kernel<8, fp32 W^T, integer widening> (rank 0)",
+                         "achieved": work / (ms / 1e3) / 1e12, "peak": peak / 1e12, "unit": "T conv+FMA/s",
+                         "frac": work / (ms / 1e3) / peak, "peak_source": psrc,
+                         "work": "nnz x N fp32->fp64 conversions + fp64 FMAs per call (incl. the top-2 merge)"},
+            "cpu_baseline": cpu,
+            "tc_3xtf32": {"docs": ns, "docs_per_s": ns / (tcm / 1e3), "ms": tcm,
+                          "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
+                                       "achieved": executed, "peak": tpeak, "unit": "TFLOP/s",
+                                       "frac": executed / tpeak, "peak_source": tsrc,
+                                       "work": "3 x 2 n N d executed TF32 flop per call, incl. split + merge"}}}
 
 
 def c4_leg(som, torch, args, local, rank, world):
-    """c4 (BASELINE.json configs[3]: 100x100 hex map, 20,000 terms) online
-    training, the first --c4-steps steps.  At N > 1 the map is neuron-sharded
-    over the ranks (dist.ShardedSOM: units u = r + P l, X replicated, the
+    """c4 (BASELINE.json configs[3]: 100x100 hex, 200,000 x 20,000, 2 epochs)
+    online training, the first --c4-steps steps.  At N > 1 the map is
+    neuron-sharded over the ranks (units u = r + N l; X replicated; the
     per-step winner exchanged inside the training kernel through peer-memory
-    mailboxes over NVLink); at N = 1 the same steps on one GPU.  Failures are
-    contained: every rank reports its status through an all-reduce and the
-    leg returns an error entry instead of stopping the bench."""
+    mailboxes over NVLink).  Beside it the exchange latency alone (a 16-unit
+    map per GPU): in-kernel mailbox vs the NCCL baseline (one step kernel +
+    ncclAllReduce(u64, min) per step, CUDA-graph replayed)."""
     import torch.distributed as dist
-    rows = cols = 100
-    d, n, steps = 20000, args.c4_docs, args.c4_steps
-    C = bank_corpus(n, d, seed=args.seed + 400)                  # identical on every rank
-    X = torch.from_numpy(C.dense()).cuda(local)
-    from synth import init_rows
-    W0 = torch.from_numpy(init_rows(C.dense(), rows * cols, args.seed + 401) if n >= rows * cols else
-                          (0.5 * bank_corpus(rows * cols, d, seed=args.seed + 402).dense()
-                           + 0.5 * C.dense().mean(0)).astype(np.float32)).cuda(local)
+    cfg = CONFIGS["c4"]
+    rows, cols, d = cfg["rows"], cfg["cols"], cfg["d"]
+    C = bank_corpus(cfg["n"], d, seed=args.seed + 400)          # identical on every rank
+    rp, ci, va = (torch.from_numpy(a).cuda(local) for a in (C.indptr, C.indices, C.data))
+    steps = args.c4_steps
     ok = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ms, err, chk = 0.0, "", 0.0
+    ms, err = 0.0, ""
+    g = k = -1
     sm = None
-    if world > 1:
-        # set-up (IPC mailboxes) and training each end in an all-reduced
-        # status, so a rank that fails never leaves the others in a collective
-        try:
-            from paper_1905_09598_b200.dist import ShardedSOM
-            sm = ShardedSOM(rows, cols, d, 1, rank, world, device=local)
-            sm.set_weights(W0)
-        except Exception as e:
-            ok[0] = 1.0
-            err = "setup: " + str(e)[:200]
-        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
-        if ok.item() > 0:
-            return {"workload": "c4 neuron-sharded training", "error": err or "set-up failed on another rank"}
     try:
-        log = torch.empty(steps, dtype=torch.int32, device="cuda")
         if world > 1:
-            dist.barrier()
-            som.som_train_online(sm.h, X, n, 2, ALPHA0, 50.0, None, args.seed, 0, steps, log)
-            ms, _, _ = som.som_last_stats(sm.h)
-            g, k = som.som_last_train_config(sm.h)
-            sm.close()
+            from paper_1905_09598_b200.dist import ShardedSOM
+            sm = ShardedSOM(rows, cols, d, cfg["topo"], rank, world, device=local)
+            h = sm.h
         else:
-            with som.SOM(rows, cols, d, 1, device=local) as m1:
-                m1.set_weights(W0)
-                som.som_train_online(m1.h, X, n, 2, ALPHA0, 50.0, None, args.seed, 0, steps, log)
-                ms, _, _ = som.som_last_stats(m1.h)
-                g, k = som.som_last_train_config(m1.h)
-        lg = log.cpu().numpy().astype(np.float64)
-        chk = float((lg * (1 + np.arange(steps) % 977)).sum())
-    except Exception as e:      # contained: reported below, never left hanging in a collective
+            h = som.som_create(rows, cols, d, cfg["topo"], local)
+        som.som_init_random_csr(h, rp, ci, va, C.n, args.seed + 1401)
+    except Exception as e:
         ok[0] = 1.0
-        err = str(e)[:200]
-        g, k = 0, -1
+        err = "setup: " + str(e)[:200]
     if world > 1:
         dist.all_reduce(ok, op=dist.ReduceOp.MAX)
     if ok.item() > 0:
-        return {"workload": "c4 neuron-sharded training", "error": err or "failed on another rank"}
+        return {"workload": "c4 training", "error": err or "set-up failed on another rank"}
+    log = torch.empty(steps, dtype=torch.int32, device="cuda")
+    try:
+        if world > 1:
+            dist.barrier()
+        som.som_train_online_csr(h, rp, ci, va, C.n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, args.seed, 0, steps,
+                                 log)
+        ms = som.som_last_stats(h)[0]
+        g, k = som.som_last_train_config(h)
+    except Exception as e:
+        ok[0] = 1.0
+        err = str(e)[:200]
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+    if sm is not None:
+        sm.close()
+    else:
+        som.som_destroy(h)
+    if ok.item() > 0:
+        return {"workload": "c4 training", "error": err or "failed on another rank"}
+    lg = log.cpu().numpy().astype(np.float64)
+    chk = float((lg * (1 + np.arange(steps) % 977)).sum())
     t = torch.tensor([ms, chk, -chk], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, consistent = float(t[0]), bool(float(t[1]) == -float(t[2]))
-    probe = exchange_probe(som, torch, args, local, rank, world)
-    return {"exchange_probe": probe,
-            "workload": f"c4: 100x100 hex, 20,000 terms, {n} docs replicated, steps [0, {steps}) of 2 epochs, "
-                        f"{'neuron-sharded over ' + str(world) + ' GPUs (in-kernel NVLink winner exchange)' if world > 1 else 'one GPU'}",
-            "samples_per_s": steps / (ms_max / 1000.0), "us_per_step": 1000.0 * ms_max / steps,
+    return {"workload": f"c4: 100x100 hex, {C.n} CSR docs x {d} terms (replicated), steps [0, {steps}) of "
+                        f"{cfg['epochs']} epochs, {'neuron-sharded over ' + str(world) + ' GPUs' if world > 1 else '1 GPU'}",
+            "samples_per_s": steps / (float(t[0]) / 1e3), "us_per_step": 1e3 * float(t[0]) / steps,
             "units_per_gpu": (rows * cols + world - 1) // world, "grid": g, "kernel": k,
             "scaling": "strong (one map, units split over the ranks)",
-            "bmu_log_identical_on_all_ranks": consistent}
+            "bmu_log_identical_on_all_ranks": bool(float(t[1]) == -float(t[2])),
+            "exchange_probe": exchange_probe(som, torch, args, local, rank, world)}
+
+
+def exchange_probe(som, torch, args, local, rank, world):
+    """Per-step cost of the winner exchange alone: 16 units per GPU, d = 64
+    (negligible work), 20,000 steps.  mailbox: the in-kernel exchange (at
+    N = 1 the in-GPU all-gather only); nccl: one step kernel + one
+    ncclAllReduce(u64, min) per step (libsom's communicator)."""
+    import torch.distributed as dist
+    from synth import uniform_matrix
+    side_c, steps, n = 16, 20000, 2000
+    X = torch.from_numpy(uniform_matrix(n, 64, args.seed + 700)).cuda(local)
+    W0 = torch.from_numpy(uniform_matrix(world * side_c, 64, args.seed + 701)).cuda(local)
+    out = {"units_per_gpu": side_c, "d": 64, "steps": steps}
+    for mode in ("mailbox", "nccl"):
+        ok = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ms = 0.0
+        h = None
+        try:
+            h = som.som_create(world, side_c, 64, 1, local)
+            if mode == "nccl":
+                from paper_1905_09598_b200 import dist as sdist
+                sdist.init_nccl(h, rank, world, som.SOM_SHARD_NEURONS)
+                som.som_set_exchange(h, som.SOM_XCHG_NCCL)
+            elif world > 1:
+                from paper_1905_09598_b200.dist import exchange_handles
+                som.som_comm_init(h, rank, world)
+                som.som_comm_set_peers_ipc(h, exchange_handles(som.som_comm_mailbox_ipc(h)))
+            som.som_set_weights(h, W0)
+            if world > 1:
+                dist.barrier()
+            st = steps if mode == "mailbox" else steps // 4
+            som.som_train_online(h, X, n, 10, ALPHA0, 8.0, None, args.seed, 0, st, None)
+            ms = som.som_last_stats(h)[0] / st
+        except Exception as e:
+            ok[0] = 1.0
+            out[mode + "_error"] = str(e)[:200]
+        if h is not None:
+            som.som_destroy(h)
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[mode + "_us_per_step"] = None if ok.item() > 0 else 1e3 * float(t[0])
+    out["what"] = ("in-GPU all-gather + cross-GPU mailbox exchange (mailbox); step kernel + NCCL all-reduce (nccl)"
+                   if world > 1 else "one GPU: in-GPU all-gather (mailbox); step kernel + world-1 NCCL all-reduce (nccl)")
+    return out
+
+
+def c2_leg(som, torch, args, local, seed):
+    """The round-1 headline for continuity: c2 (20x20 hex, 5,000 x 3,000,
+    100 epochs = 500,000 samples) in one som_fit_csr call."""
+    cfg = CONFIGS["c2"]
+    C = bank_corpus(cfg["n"], cfg["d"], seed=seed)
+    rp, ci, va = (torch.from_numpy(a).cuda(local) for a in (C.indptr, C.indices, C.data))
+    with som.SOM(cfg["rows"], cfg["cols"], cfg["d"], cfg["topo"], device=local) as m:
+        som.som_set_stream(m.h, torch.cuda.current_stream())
+        som.som_fit_csr(m.h, rp, ci, va, C.n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, seed + 1000)
+        ms = []
+        for _ in range(args.c2_steps):
+            som.som_fit_csr(m.h, rp, ci, va, C.n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, seed + 1000)
+            ms.append(som.som_last_stats(m.h)[0])
+        ph, tr = som.som_last_phases(m.h)
+        g, k = som.som_last_train_config(m.h)
+    T = cfg["epochs"] * cfg["n"]
+    return {"workload": "c2 (BASELINE configs[1]): 20x20 hex, 5,000 x 3,000, 100 epochs, som_fit_csr",
+            "samples_per_s": T / (statistics.mean(ms) / 1e3), "us_per_training_step": 1e3 * tr / T,
+            "train_kernel": k, "grid": g}
 
 
 TABLE3_PAPER_S = {16: 34.25, 32: 32.81, 64: 33.37, 128: 38.40, 256: 111.03, 512: 431.38}   # P:304-305
@@ -470,104 +545,90 @@ def table3_leg(som, torch, args, local, seed):
             "paper": "CUDASOM on a Quadro P5000, seconds: " + ", ".join(f"{k}^2 {v}" for k, v in TABLE3_PAPER_S.items())}
 
 
-def train_c3_leg(som, torch, args, local, seed):
-    """Online training in the bandwidth-bound regime: c3 (50x50 hex, 50k x 10k,
-    W = 100 MB streamed through L2/HBM every step), first `--c3-steps` steps."""
+def batch_leg(som, torch, args, local, seed, C3):
+    """Batch SOM (R27, som_train_batch_csr) on the c3 corpus, --batch-epochs
+    epochs: exact BMUs, documents bucketed by BMU, per-unit fp64 sums, lattice
+    kernel contraction."""
     cfg = CONFIGS["c3"]
-    n, d, N = cfg["n"], cfg["d"], cfg["rows"] * cfg["cols"]
-    T = cfg["epochs"] * n
-    steps = args.c3_steps
-    C = bank_corpus(n, d, seed=seed + 300)
-    X = torch.from_numpy(C.dense()).cuda()
-    mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
-    som.som_set_stream(mm.h, torch.cuda.current_stream())
-    som.som_init_random(mm.h, X, n, seed + 1300)
-    log = torch.empty(steps, dtype=torch.int32, device="cuda")
-    som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, 2000, None)   # warm-up
-    som.som_init_random(mm.h, X, n, seed + 1300)
-    som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, steps, log)
-    ms, _, _ = som.som_last_stats(mm.h)
-    g, kern = som.som_last_train_config(mm.h)
-    H = updated_units(cfg["rows"], cfg["cols"], cfg["topo"], log.cpu().numpy(), 0, T, cfg["sigma0"])
-    algo = float(4.0 * N * d * steps + 4.0 * d * H.sum() + 4.0 * d * steps)   # read W, write updated rows, read x
-    gbps = algo / (ms / 1000.0) / 1e9
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-        hbm = float(json.load(f)["hbm_gbs"])
-    l2, l2_src = 12144.0, "measured L2 read+write bandwidth at a 96 MB footprint (profiles/probes_r01.json l2_rw_GBps)"
-    try:
-        with open(os.path.join(ROOT, "profiles", "probes_r01.json")) as f:
-            l2 = float(json.load(f)["l2_rw_GBps"]["96"])
-    except Exception:
-        l2_src += " (file missing: fallback value)"
-    # late window (radius near sigma_min: few units updated): the dense kernel
-    # still reads all of W per step; the CSR kernel's sparse distance reads
-    # only the non-zero columns (SURVEY NEXT-1)
-    late = {}
-    t0 = T - steps
-    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
-    for name, csr in (("dense", False), ("csr", True)):
-        som.som_init_random(mm.h, X, n, seed + 1300)
-        if csr:
-            som.som_train_online_csr(mm.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, t0, T, None)
-        else:
-            som.som_train_online(mm.h, X, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, t0, T, None)
-        lms, _, _ = som.som_last_stats(mm.h)
-        late[name] = {"us_per_step": 1000.0 * lms / steps, "kernel": som.som_last_train_config(mm.h)[1]}
-    mm.close()
-    return {"workload": f"c3: {cfg['rows']}x{cfg['cols']} hex, {n} x {d}, steps [0, {steps}) of T = {T}",
-            "samples_per_s": steps / (ms / 1000.0), "us_per_step": 1000.0 * ms / steps,
-            "mean_updated_units": float(H.mean()),
-            "late_window": {"steps": f"[{t0}, {T})", **late},
-            "roofline": {"bound": "l2", "kernel": f"som_train_tma_kernel / som_train_glb_kernel (kernel id {kern}), G={g}",
-                         "achieved": gbps, "peak": l2, "unit": "GB/s", "frac": gbps / l2,
-                         "peak_source": l2_src,
-                         "hbm_frac": gbps / hbm,
-                         "work": "4*N*d read + 4*H_t*d written + 4*d per sample (H_t from the BMU log); W (100 MB) "
-                                 "is kept in L2 by a persisting window, so L2 read+write bandwidth is the bound "
-                                 "(hbm_frac: the same bytes against the HBM copy bandwidth)"}}
+    rp, ci, va = C3
+    n = rp.numel() - 1
+    with som.SOM(cfg["rows"], cfg["cols"], cfg["d"], cfg["topo"], device=local) as m:
+        som.som_set_stream(m.h, torch.cuda.current_stream())
+        som.som_init_random_csr(m.h, rp, ci, va, n, seed + 301)
+        som.som_train_batch_csr(m.h, rp, ci, va, n, 1, cfg["sigma0"], None, None)     # warm-up
+        som.som_init_random_csr(m.h, rp, ci, va, n, seed + 301)
+        som.som_train_batch_csr(m.h, rp, ci, va, n, args.batch_epochs, cfg["sigma0"], None, None)
+        ms, units, launches = som.som_last_stats(m.h)
+    return {"workload": f"c3 corpus: 50x50 hex, {n} CSR docs x {cfg['d']} terms, {args.batch_epochs} batch epochs",
+            "docs_per_s": units / (ms / 1e3), "ms_per_epoch": ms / args.batch_epochs, "launches": launches}
 
 
 # ------------------------------------------------------------- oracle legs
-def oracle_train_rate(cfg, X, W0, seed, steps):
+def oracle_train_rate(cfg, X, W0, seed, steps, threads=None):
     import oracle
     T = cfg["epochs"] * cfg["n"]
-    t0 = time.perf_counter()
-    oracle.train_online(W0, cfg["rows"], cfg["cols"], cfg["topo"], X, cfg["epochs"], ALPHA0, cfg["sigma0"],
-                        seed, t_begin=0, t_end=min(steps, T))
-    dt = time.perf_counter() - t0
-    return min(steps, T) / dt, dt, oracle.num_threads()
+    nt = oracle.num_threads()
+    if threads:
+        oracle.set_num_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        oracle.train_online(W0, cfg["rows"], cfg["cols"], cfg["topo"], X, cfg["epochs"], ALPHA0, cfg["sigma0"],
+                            seed, t_begin=0, t_end=min(steps, T))
+        dt = time.perf_counter() - t0
+        used = oracle.num_threads()
+    finally:
+        oracle.set_num_threads(nt)
+    return min(steps, T) / dt, dt, used
+
+
+def corpus_seed(name, seed):
+    return seed + 300 if name == "c3" else seed
+
+
+def oracle_inputs(name, seed):
+    """The oracle's dense copy of the same corpus (seeded) and a seeded row init."""
+    from synth import init_rows
+    cfg = CONFIGS[name]
+    X = bank_corpus(cfg["n"], cfg["d"], seed=corpus_seed(name, seed)).dense()
+    return X, init_rows(X, cfg["rows"] * cfg["cols"], seed + 1300)
+
+
+REF_STEPS = {"c1": 2000, "c2": 400, "c3": 300}   # oracle steps per reference-arm step (~3-6 s each on 16 cores)
 
 
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the oracle (plain fp64 CPU SOM), as it
+    stands, on the host cores, on bounded samples of the same workload."""
     if rank != 0:
         return
     import oracle
-    cfg, C = workload(args.config, args.seed, args.epochs)
-    X = C.dense()
-    from synth import init_rows
-    W0 = init_rows(X, cfg["rows"] * cfg["cols"], args.seed + 1000)
-    steps_per = {"c1": 2000, "c2": 400, "c3": 10}[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.epochs is not None:
+        cfg["epochs"] = args.epochs
+    X, W0 = oracle_inputs(args.config, args.seed)
+    steps_per = REF_STEPS[args.config]
     for _ in range(args.warmup):
-        oracle_train_rate(cfg, X, W0, args.seed, max(1, steps_per // 4))
-    rates, secs = [], 0.0
+        oracle_train_rate(cfg, X, W0, args.seed, max(1, steps_per // 10))
+    secs = 0.0
     for _ in range(args.steps):
-        r, dt, nt = oracle_train_rate(cfg, X, W0, args.seed, steps_per)
-        rates.append(r)
+        _, dt, nt = oracle_train_rate(cfg, X, W0, args.seed, steps_per)
         secs += dt
     v = args.steps * steps_per / secs
     sample = (f"first {steps_per} of {cfg['epochs'] * cfg['n']} training steps of {args.config} per step "
-              f"(fp64 oracle, OpenMP over units)")
+              f"(fp64 oracle, OpenMP over units, {nt} threads)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": args.config, **cfg},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded bank-shaped TF-IDF, synth/corpus.py)",
+            "config": config_dict(args.config, cfg, world),
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": nt, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# -------------------------------------------------------------- B200 leg
+# -------------------------------------------------------------- B200 arm
 def run_b200(args, rank, world, local):
+    c5 = c5_corpus(args.c5_docs, rank, world) if args.c5_docs > 0 else None    # host processes before CUDA
     import torch
     import torch.distributed as dist
 
@@ -580,173 +641,207 @@ def run_b200(args, rank, world, local):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    seed = args.seed + rank                     # independent problem per rank
-    cfg, C = workload(args.config, seed, args.epochs)
+    seed = args.seed
+    cfg = dict(CONFIGS[args.config])
+    if args.epochs is not None:
+        cfg["epochs"] = args.epochs
     n, d, N = cfg["n"], cfg["d"], cfg["rows"] * cfg["cols"]
     T = cfg["epochs"] * n
-    X_host = torch.from_numpy(C.dense()).pin_memory()
-    X = X_host.cuda()
+    C = bank_corpus(n, d, seed=corpus_seed(args.config, seed))    # identical on every rank
+    rp, ci, va = (torch.from_numpy(a).cuda(local) for a in (C.indptr, C.indices, C.data))
     stream = torch.cuda.current_stream()
-    m = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
-    som.som_set_stream(m.h, stream)
-    # mapping / QE / TE of the step through the exact sparse identity (R25):
-    # the TF-IDF rows are put in CSR form on the device
-    som.som_set_map_precision(m.h, som.SOM_MAP_SPARSE_F64)
-    b1 = torch.empty(n, dtype=torch.int32, device="cuda")
-    b2 = torch.empty(n, dtype=torch.int32, device="cuda")
-    d1 = torch.empty(n, dtype=torch.float32, device="cuda")
-    U = torch.empty(N, dtype=torch.float32, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
-    sched = som.som_schedule_default()
+    init_seed = seed + 1000
 
-    def one_step(Xs, b1s, b2s, d1s, Us):
-        """The whole hot path once; returns per-phase kernel ms and launches."""
-        ph, launches = {}, 0
-        som.som_init_random(m.h, Xs, n, seed + 1000)
-        ms, _, l = som.som_last_stats(m.h)
-        launches += 1 if Xs.is_cuda else 0
-        som.som_train_online(m.h, Xs, n, cfg["epochs"], ALPHA0, cfg["sigma0"], sched, seed, 0, -1, None)
-        ph["train_ms"], _, l = som.som_last_stats(m.h)
-        launches += l
-        som.som_map(m.h, Xs, n, b1s, b2s, d1s)
-        ph["map_ms"], _, l = som.som_last_stats(m.h)
-        launches += l
-        qe, te = som.som_errors(m.h, Xs, n)
-        ph["errors_ms"], _, l = som.som_last_stats(m.h)
-        launches += l
-        som.som_umatrix(m.h, Us)
-        ph["umatrix_ms"], _, l = som.som_last_stats(m.h)
-        launches += l
-        return ph, launches, qe, te
+    if world == 1:
+        m = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+        som.som_set_stream(m.h, stream)
+        b1 = torch.empty(n, dtype=torch.int32, device="cuda")
+        b2 = torch.empty(n, dtype=torch.int32, device="cuda")
+        d1 = torch.empty(n, dtype=torch.float32, device="cuda")
+        U = torch.empty(N, dtype=torch.float32, device="cuda")
 
-    for _ in range(args.warmup):
-        one_step(X, b1, b2, d1, U)
+        def one_step(ins, outs):
+            qe, te = som.som_fit_csr(m.h, *ins, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, init_seed, *outs)
+            ph, train_ms = som.som_last_phases(m.h)
+            return {"phase_ms": dict(zip(["init", "train", "map", "errors", "umatrix"], ph)),
+                    "train_kernel_ms": train_ms, "launches": som.som_last_stats(m.h)[2], "qe": qe, "te": te}
+        dev_in, dev_out = (rp, ci, va), (b1, b2, d1, U)
+    else:
+        from paper_1905_09598_b200 import dist as sdist
+        sm = sdist.ShardedSOM(cfg["rows"], cfg["cols"], d, cfg["topo"], rank, world, device=local)
+        som.som_set_stream(sm.h, stream)
+        md = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
+        som.som_set_stream(md.h, stream)
+        sdist.init_nccl(md.h, rank, world, som.SOM_SHARD_DOCS)
+        lo, hi = sdist.shard_range(n, rank, world)
+        srp = (rp[lo:hi + 1] - rp[lo]).contiguous()
+        sci, sva = ci[int(C.indptr[lo]):int(C.indptr[hi])], va[int(C.indptr[lo]):int(C.indptr[hi])]
+        ns = hi - lo
+        b1 = torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")
+        b2 = torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")
+        d1 = torch.empty(max(ns, 1), dtype=torch.float32, device="cuda")
+        U = torch.empty(N, dtype=torch.float32, device="cuda")
+        Wfull = torch.zeros(N, d, dtype=torch.float32, device="cuda")
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+        def one_step(ins, outs):
+            evs[0].record(stream)
+            som.som_init_random_csr(sm.h, rp, ci, va, n, init_seed)
+            evs[1].record(stream)
+            dist.barrier()
+            som.som_train_online_csr(sm.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, -1, None)
+            train_ms = som.som_last_stats(sm.h)[0]
+            dist.barrier()
+            evs[2].record(stream)
+            Wfull.zero_()
+            som.som_get_weights(sm.h, Wfull)                 # own rows; all-reduce assembles the map
+            dist.all_reduce(Wfull)
+            md.set_weights(Wfull)
+            som.som_map_csr(md.h, srp, sci, sva, ns, b1, b2, d1)
+            evs[3].record(stream)
+            qe, te = som.som_errors_csr(md.h, srp, sci, sva, ns)   # NCCL-reduced inside libsom
+            evs[4].record(stream)
+            som.som_umatrix(md.h, U)
+            evs[5].record(stream)
+            torch.cuda.synchronize()
+            ph = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
+            return {"phase_ms": dict(zip(["init", "train", "map (gather W + shard)", "errors", "umatrix"], ph)),
+                    "train_kernel_ms": train_ms, "launches": 0, "qe": qe, "te": te}
+        dev_in, dev_out = None, None
+
+    for _ in range(max(3, args.warmup)):
+        one_step(dev_in, dev_out)
     torch.cuda.synchronize()
 
-    # ---- timed region: device resident inputs
+    # ---- timed region: inputs resident in HBM
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    phases, launches = [], 0
+    infos = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
-        w0 = time.perf_counter()
         for i in range(args.steps):
-            flush.zero_()                      # L2 flush between timed steps (not timed)
+            flush.zero_()                                # L2 flush between timed steps (not timed)
             ev[i][0].record(stream)
-            ph, l, qe, te = one_step(X, b1, b2, d1, U)
+            infos.append(one_step(dev_in, dev_out))
             ev[i][1].record(stream)
-            phases.append(ph)
-            launches += l
         torch.cuda.synchronize()
-        wall = time.perf_counter() - w0
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_max = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     total_ms = float(t_max.item())
-    value = world * args.steps * T / (total_ms / 1000.0)
+    value = args.steps * T / (total_ms / 1e3)
 
-    # ---- e2e: same step through the C ABI with pinned HOST buffers
-    b1h = torch.empty(n, dtype=torch.int32).pin_memory()
-    b2h = torch.empty(n, dtype=torch.int32).pin_memory()
-    d1h = torch.empty(n, dtype=torch.float32).pin_memory()
-    Uh = torch.empty(N, dtype=torch.float32).pin_memory()
-    Wh = torch.empty(N, d, dtype=torch.float32).pin_memory()
-    e2e_ms = []
-    for i in range(max(1, min(args.steps, 3))):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        one_step(X_host, b1h, b2h, d1h, Uh)
-        som.som_get_weights(m.h, Wh)
-        torch.cuda.synchronize()
-        e2e_ms.append(1000 * (time.perf_counter() - t0))
-    e2e_t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    xb = n * d * 4
-    h2d = 3 * xb                               # X staged by train, map and errors
-    d2h = n * 4 * 2 + n * 4 + N * 4 + N * d * 4 + 16
+    # ---- e2e: the same call with pinned HOST inputs and host outputs
+    e2e = None
+    if world == 1:
+        hin = tuple(torch.from_numpy(a).pin_memory() for a in (C.indptr, C.indices, C.data))
+        hout = (torch.empty(n, dtype=torch.int32).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
+                torch.empty(n, dtype=torch.float32).pin_memory(), torch.empty(N, dtype=torch.float32).pin_memory())
+        e2e_ms = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            one_step(hin, hout)
+            torch.cuda.synchronize()
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+        h2d = int(C.indptr.nbytes + C.indices.nbytes + C.data.nbytes)
+        d2h = 12 * n + 4 * N + 16
+        e2e = {"value": T / (statistics.mean(e2e_ms) / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "what": "som_fit_csr with pinned host CSR arrays (staged once per call) and host outputs (bmu1, bmu2, "
+                       "D1, U, QE, TE), wall clock per call"}
 
-    # ---- roofline of the dominant kernel (the persistent training kernel)
-    train_ms = statistics.mean(p["train_ms"] for p in phases)
-    flop_per_sample = 3.0 * N * d               # fp64 distance: sub + fma per element (R10)
-    achieved = flop_per_sample * T / (train_ms / 1000.0) / 1e12
-    peak, peak_src = train_peak_tflops()
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+    # ---- roofline of the dominant kernel (the training kernel of the step)
+    train_ms = statistics.mean(i["train_kernel_ms"] for i in infos)
+    roof = None
+    g_used = k_used = -1
+    if world == 1:
+        g_used, k_used = som.som_last_train_config(m.h)
+        # the BMU log of the same (deterministic) training, untimed, for H_t
+        log = torch.empty(T, dtype=torch.int32, device="cuda")
+        som.som_init_random_csr(m.h, rp, ci, va, n, init_seed)
+        som.som_train_online_csr(m.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, -1, log)
+        H = updated_units(cfg["rows"], cfg["cols"], cfg["topo"], log.cpu().numpy(), 0, T, cfg["sigma0"])
+        nnz_x = C.nnz / n
+        sparse = k_used in (4, 9)
+        algo = train_bytes(N, d, nnz_x, H, sparse)
+        gbps = algo / (train_ms / 1e3) / 1e9
+        l2, l2src = l2_peak_gbs(96)
+        hbm, hsrc = hbm_peak_gbs()
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj.get("bytes_per_launch")
+        kname = {3: "som_train_tma_kernel (dense rows, W streamed)", 4: "som_train_csr_tma_kernel (sparse distances, "
+                 "W streamed through L2)", 2: "som_train_reg_kernel (W in registers)"}.get(k_used, f"kernel {k_used}")
+        roof = {"bound": "l2", "kernel": f"{kname}, G={g_used}", "achieved": gbps, "peak": l2, "unit": "GB/s",
+                "frac": gbps / l2, "traffic": traffic, "peak_source": l2src, "hbm_frac": gbps / hbm,
+                "hbm_peak_source": hsrc,
+                "work": ("per step: 8 H_t d (read + write the updated rows) + 4 nnz(x_t) (N - H_t) (the sparse "
+                         "distance's gathered weights) + 8 nnz(x_t) bytes" if sparse else
+                         "per step: 4 N d (read W) + 4 H_t d (write updated rows) + 4 d bytes") +
+                        f"; H_t from the BMU log (mean {H.mean():.0f} of {N} units), {algo / T / 1e6:.1f} MB/step",
+                "kernel_ms": train_ms, "kernel_share_of_step": train_ms / (total_ms / args.steps)}
 
-    g_used, k_used = som.som_last_train_config(m.h)
-    kname = {0: "som_train_kernel (W global)", 1: "som_train_kernel (W smem)",
-             2: "som_train_reg_kernel (W registers)", 6: "som_train_spec_kernel (W registers, overlapped exchange)",
-             7: "som_train_spec_kernel then som_train_reg_kernel (W registers; one call, two launches)"}.get(k_used, "?")
-    mapping = mapping_leg(som, torch, args, local, seed, world, rank) if args.map_docs > 0 else None
-    train_c3 = train_c3_leg(som, torch, args, local, seed) if args.c3_steps > 0 else None
-    table3 = table3_leg(som, torch, args, local, seed) if args.table3_steps > 0 else None
-    batch = batch_leg(som, torch, args, local, seed) if args.batch_epochs > 0 else None
-    c4 = c4_leg(som, torch, args, local, rank, world) if args.c4_steps > 0 else None
+    # ---- secondary legs
+    legs = {}
+    if c5 is not None:
+        legs["c5_mapping"] = c5_leg(som, torch, args, local, rank, world, c5)
+    if args.c4_steps > 0:
+        legs["c4_training"] = c4_leg(som, torch, args, local, rank, world)
+    if world == 1:
+        if args.c2_steps > 0:
+            legs["c2"] = c2_leg(som, torch, args, local, seed)
+        if args.table3_steps > 0:
+            legs["table3"] = table3_leg(som, torch, args, local, seed)
+        if args.batch_epochs > 0 and args.config == "c3":
+            legs["batch_som"] = batch_leg(som, torch, args, local, seed, (rp, ci, va))
 
     if rank != 0:
-        dist.destroy_process_group() if world > 1 else None
+        if world > 1:
+            dist.destroy_process_group()
         return
 
     cpu = None
     if not args.no_baseline:
-        import oracle
-        from synth import init_rows
-        Xn = X_host.numpy()
-        W0 = init_rows(Xn, N, seed + 1000)
-        steps_s = {"c1": 20000, "c2": 50000, "c3": 200}[args.config]   # ~10 s of host work (c2)
-        r, dt, nt = oracle_train_rate(cfg, Xn, W0, seed, steps_s)
+        X, W0 = oracle_inputs(args.config, seed)
+        steps_s = {"c1": 2000, "c2": 20000, "c3": 1500}[args.config]        # ~10 s of host work
+        r, dt, nt = oracle_train_rate(cfg, X, W0, seed, steps_s)
         cpu = {"value": r, "unit": "samples/s", "cores": nt, "kind": "oracle",
-               "sample": f"first {steps_s} of {T} training steps of {args.config} ({dt:.1f} s, fp64 oracle, "
-                         f"OpenMP over units)"}
-        # SURVEY §8.D: the oracle on one core as well (a shorter prefix)
-        steps_1 = max(1, steps_s // 25)
-        oracle.set_num_threads(1)
-        try:
-            r1, dt1, _ = oracle_train_rate(cfg, Xn, W0, seed, steps_1)
-        finally:
-            oracle.set_num_threads(nt)
+               "sample": f"first {steps_s} of {T} training steps of {args.config} ({dt:.1f} s, fp64 oracle, OpenMP "
+                         f"over units); the mapping/QE/U-matrix share of the step is < 1 % on both sides"}
+        steps_1 = {"c1": 400, "c2": 1000, "c3": 60}[args.config]
+        r1, dt1, _ = oracle_train_rate(cfg, X, W0, seed, steps_1, threads=1)
         cpu["single_core"] = {"value": r1, "unit": "samples/s", "cores": 1,
                               "sample": f"first {steps_1} training steps ({dt1:.1f} s)"}
+        cpu["gpu_over_oracle"] = {"all_cores": value / r, "single_core": value / r1}
 
-    ph_mean = {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
+    ph_mean = {k: statistics.mean(i["phase_ms"][k] for i in infos) for k in infos[0]["phase_ms"]}
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64-acc/f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64-acc/f32",
         "data": "synthetic (seeded bank-shaped TF-IDF, synth/corpus.py)",
-        "config": {"workload": args.config, "map": f"{cfg['rows']}x{cfg['cols']} {'hex' if cfg['topo'] else 'rect'}",
-                   "docs": n, "terms": d, "epochs": cfg["epochs"], "samples_per_step": T,
-                   "alpha0": ALPHA0, "sigma0": cfg["sigma0"], "cutoff": 1e-4, "parallelism": f"replicas{world}",
-                   "l2": "flushed between timed steps (256 MB write)",
-                   "mapping": "exact sparse identity (SOM_MAP_SPARSE_F64, R25)"},
-        "secondary": {"map_docs_per_s": n / (ph_mean["map_ms"] / 1000.0),
-                      "train_samples_per_s_kernel": T / (train_ms / 1000.0),
-                      "us_per_training_step": 1000.0 * train_ms / T, "phase_ms": ph_mean,
-                      "qe": qe, "te": te, "wall_s": wall},
-        "e2e": {"value": world * T / (float(e2e_t.item()) / 1000.0), "unit": "samples/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "mapping": mapping,
-        "train_c3": train_c3,
-        "table3": table3,
-        "batch_som": batch,
-        "train_c4": c4,
-        "roofline": {"bound": "alu", "kernel": f"{kname}, G={g_used}", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_src,
-                     "work": "3*N*d fp64 flop per sample (difference + fused square-accumulate)"},
+        "config": config_dict(args.config, cfg, world),
+        "secondary": {"map_docs_per_s": n / (ph_mean[list(ph_mean)[2]] / 1e3),
+                      "train_samples_per_s_kernel": T / (train_ms / 1e3),
+                      "us_per_training_step": 1e3 * train_ms / T, "phase_ms": ph_mean,
+                      "qe": infos[-1]["qe"], "te": infos[-1]["te"], "train_kernel": k_used, "grid": g_used},
+        "e2e": e2e,
+        "gpu_launches": infos[-1]["launches"] * args.steps if world == 1 else None,
+        "roofline": roof,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "paper_context": PAPER_44X,
+        **legs,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -114,6 +114,10 @@ som_status som_get_weights(som_ctx *h, float *w);
  * otherwise (R18; the paper's PCA-plane init, is NEXT-3). */
 som_status som_init_random(som_ctx *h, const float *X, int64_t n, uint64_t seed);
 
+/* som_init_random on CSR rows (the drawn rows densified into W). */
+som_status som_init_random_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col, const float *val,
+                               int64_t n, uint64_t seed);
+
 /* Online ("standard") SOM training: for each step
  * t in [t_begin, t_end) of T = epochs * n steps (R7):
  *   i_t   = sample index: t-th SplitMix64(seed) output mapped to [0,m) (R8)
@@ -348,6 +352,25 @@ som_status som_errors_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col,
  * |w_u - w_v|_2 (fp64 accumulation, fp32 result), 0 with no neighbour.
  * U: N floats, host or device. */
 som_status som_umatrix(som_ctx *h, float *U);
+
+/* The whole hot path in one call: som_init_random
+ * (init_seed, R18) + som_train_online over the full schedule [0, epochs*n)
+ * + mapping of all n rows (som_map) + QE / TE from those mapping outputs
+ * (som_errors, no second mapping pass) + som_umatrix.  The input is staged
+ * to the device once per call.  bmu1, bmu2, d2 (n), qe, te, U (N): nullable
+ * outputs, host or device.  Same results as the individual calls.
+ * som_last_stats reports the whole call; som_last_phases the split. */
+som_status som_fit(som_ctx *h, const float *X, int64_t n, int32_t epochs, double alpha0, double sigma0,
+                   const som_schedule *s, uint64_t seed, uint64_t init_seed, int32_t *bmu1, int32_t *bmu2,
+                   float *d2, double *qe, double *te, float *U);
+som_status som_fit_csr(som_ctx *h, const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
+                       int32_t epochs, double alpha0, double sigma0, const som_schedule *s, uint64_t seed,
+                       uint64_t init_seed, int32_t *bmu1, int32_t *bmu2, float *d2, double *qe, double *te,
+                       float *U);
+/* Device time (ms) of the phases of the last som_fit call: [0] staging +
+ * init, [1] training, [2] mapping, [3] QE/TE, [4] U-matrix and output
+ * copies; *train_kernel_ms (nullable) = the training kernels alone. */
+som_status som_last_phases(som_ctx *h, double *ms5, double *train_kernel_ms);
 
 /* Use the caller's CUDA stream (cudaStream_t as void*; NULL = the
  * handle's own stream).  The caller keeps ownership of the stream. */

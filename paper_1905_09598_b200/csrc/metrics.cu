@@ -101,7 +101,24 @@ __global__ void gather_rows_kernel(const float* X, const int64_t* idx, int dim, 
     for (int k = threadIdx.x; k < dim; k += blockDim.x) dst[k] = src[k];
 }
 
+// the CSR rows idx[u] densified into W row u
+__global__ void gather_csr_rows_kernel(const int64_t* rowptr, const int32_t* col, const float* val,
+                                       const int64_t* idx, int dim, float* W) {
+    const int u = blockIdx.x;
+    float* dst = W + (int64_t)u * dim;
+    for (int k = threadIdx.x; k < dim; k += blockDim.x) dst[k] = 0.0f;
+    __syncthreads();
+    const int64_t i = idx[u];
+    for (int64_t p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) dst[col[p]] = val[p];
+}
+
 }  // namespace
+
+cudaError_t launch_gather_csr_rows(const int64_t* rowptr, const int32_t* col, const float* val, const int64_t* idx,
+                                   int N, int dim, float* W, cudaStream_t st) {
+    gather_csr_rows_kernel<<<N, 256, 0, st>>>(rowptr, col, val, idx, dim, W);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_errors(const int32_t* bmu1, const int32_t* bmu2, const float* d2, const uint8_t* keep, int64_t n,
                           int rows, int cols, int topo, double* partial, unsigned long long* partial_cnt, int nblocks,

@@ -220,7 +220,7 @@ void som_destroy(som_ctx* h) {
     som_comm_release(h);
     for (DevBuf* b : {&h->xin, &h->xin2, &h->xin3, &h->keys, &h->outs, &h->red, &h->ftab, &h->log, &h->xchg, &h->dense,
                       &h->utab, &h->wsplit, &h->xsplit, &h->wt64, &h->bbuf, &h->bS, &h->bnum, &h->up, &h->up2,
-                      &h->rflags, &h->rmap, &h->nstep})
+                      &h->rflags, &h->rmap, &h->nstep, &h->tcsr, &h->tcsr2, &h->fitx, &h->fitx2, &h->fitx3})
         b->release();
     if (h->W) cudaFree(h->W);
     for (int p = 0; p < kMaxRanks; ++p)
@@ -263,12 +263,14 @@ som_status som_get_weights(som_ctx* h, float* w) {
     return SOM_OK;
 }
 
-som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed) {
-    CHECK_HANDLE(h);
-    if (!X) return fail(SOM_EINVAL, "null X");
-    if (n < 1) return fail(SOM_EEMPTY, "n = 0");
+}  // extern "C"
+
+namespace {
+// R18: the rows of the initial codebook — N draws from SplitMix64(seed),
+// without replacement (Floyd) when N <= n; a neuron-sharded handle keeps the
+// draws of its own units
+std::vector<int64_t> init_indices(const som_ctx* h, int64_t n, uint64_t seed) {
     const int N = h->N;
-    invalidate_w_caches(h);
     std::vector<int64_t> idx((size_t)N);
     if (N <= n) {
         // Floyd's sampling without replacement, draws from SplitMix64(seed)
@@ -284,9 +286,20 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
     } else {
         for (int u = 0; u < N; ++u) idx[(size_t)u] = (int64_t)mulhi_host(splitmix64_at(seed, u), (uint64_t)n);
     }
-    // a neuron-sharded handle keeps the draws of its own units
     std::vector<int64_t> mine((size_t)h->NL);
     for (int l = 0; l < h->NL; ++l) mine[(size_t)l] = idx[(size_t)h->rank + (size_t)h->world * l];
+    return mine;
+}
+}  // namespace
+
+extern "C" {
+
+som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed) {
+    CHECK_HANDLE(h);
+    if (!X) return fail(SOM_EINVAL, "null X");
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0");
+    invalidate_w_caches(h);
+    const std::vector<int64_t> mine = init_indices(h, n, seed);
     const int NL = h->NL;
     const size_t rowb = sizeof(float) * (size_t)h->dim;
     if (is_device_ptr(X)) {
@@ -299,6 +312,23 @@ som_status som_init_random(som_ctx* h, const float* X, int64_t n, uint64_t seed)
             std::memcpy(rowsbuf.data() + (size_t)l * h->dim, X + mine[(size_t)l] * h->dim, rowb);
         CK(cudaMemcpyAsync(h->W, rowsbuf.data(), rowb * (size_t)NL, cudaMemcpyHostToDevice, h->stream));
     }
+    CK(cudaStreamSynchronize(h->stream));
+    return SOM_OK;
+}
+
+som_status som_init_random_csr(som_ctx* h, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n,
+                               uint64_t seed) {
+    CHECK_HANDLE(h);
+    if (n < 1) return fail(SOM_EEMPTY, "n = 0");
+    CsrIn csr{};
+    som_status st = stage_csr(h, rowptr, col, val, n, &csr);
+    if (st) return st;
+    invalidate_w_caches(h);
+    const std::vector<int64_t> mine = init_indices(h, n, seed);
+    CK(h->keys.ensure(sizeof(int64_t) * (size_t)h->NL, h->stream));
+    CK(cudaMemcpyAsync(h->keys.p, mine.data(), sizeof(int64_t) * (size_t)h->NL, cudaMemcpyHostToDevice, h->stream));
+    CK(launch_gather_csr_rows(csr.rowptr, csr.col, csr.val, (const int64_t*)h->keys.p, h->NL, h->dim, h->W,
+                              h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return SOM_OK;
 }

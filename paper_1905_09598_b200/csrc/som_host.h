@@ -106,6 +106,8 @@ struct som_ctx {
     int nccl_rank = 0, nccl_world = 1;
     int xchg_mode = 0;      // SOM_XCHG_MAILBOX / SOM_XCHG_NCCL
     DevBuf nstep;           // NCCL step path: keys [3] u64 | reduce scratch
+    DevBuf tcsr, tcsr2;     // dense rows put in CSR form for the training kernels: cnt | rowptr | temp, col | val
+    DevBuf fitx, fitx2, fitx3;   // som_fit: the input staged once per call
     bool wt_valid = false, wt_f32 = false, wt_nonneg = false;
     int wt_J = 0;
     // decay-table cache
@@ -117,6 +119,8 @@ struct som_ctx {
     double last_ms = 0;
     int64_t last_units = 0;
     int last_launches = 0;
+    double last_phase_ms[5] = {};   // som_fit: stage+init, train, map, errors, U-matrix (+ copies)
+    double last_train_ms = 0;       // som_fit: the training kernels alone
 };
 
 #define CK(call)                                                                              \

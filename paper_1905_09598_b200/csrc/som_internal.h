@@ -326,5 +326,7 @@ cudaError_t launch_umatrix(const float* W, int rows, int cols, int topo, int dim
                            cudaStream_t st);
 cudaError_t launch_gather_rows(const float* X, const int64_t* idx, int N, int dim, float* W,
                                cudaStream_t st);
+cudaError_t launch_gather_csr_rows(const int64_t* rowptr, const int32_t* col, const float* val, const int64_t* idx,
+                                   int N, int dim, float* W, cudaStream_t st);
 
 }  // namespace som

@@ -208,6 +208,40 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         smem = sizeof(float) * 3 * (size_t)a.dimp +
                sizeof(double) * ((size_t)a.dimp + a.rows + (a.topo == 0 ? a.cols : 2 * a.cols));
     }
+    // Dense TF-IDF rows where W streams from global memory: put the rows in
+    // CSR form on the device once per call (count, scan, fill) and take the
+    // sparse-distance kernel when they are sparse (<= 1.5 % of the terms
+    // set; SOM_TRAIN_DENSE_CSR=0 keeps the dense kernels).  Same results: the
+    // CSR kernels follow the same contract (R10 via R25) and are
+    // parity-tested against the dense oracle.
+    CsrIn auto_csr{};
+    bool dense_csr = true;
+    if (const char* e = std::getenv("SOM_TRAIN_DENSE_CSR")) dense_csr = std::atoi(e) != 0;
+    if (!csr && dense_csr && !use_small && !use_reg && !a.w_smem && a.x_vec4 && h->train_mode == SOM_TRAIN_AUTO &&
+        h->xchg_mode != SOM_XCHG_NCCL) {
+        const size_t tb = dense_csr_temp_bytes(n);
+        CK(h->tcsr.ensure(sizeof(int64_t) * 2 * ((size_t)n + 1) + tb + 256, h->stream));
+        int64_t* cnt = (int64_t*)h->tcsr.p;
+        int64_t* rp = cnt + n + 1;
+        void* temp = (void*)(((uintptr_t)(rp + n + 1) + 255) & ~(uintptr_t)255);
+        CK(launch_dense_rowptr((const float*)Xd, n, h->dim, cnt, rp, temp, tb, h->stream));
+        int64_t nnz = 0;
+        CK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if ((double)nnz <= 0.015 * (double)n * h->dim) {
+            CK(h->tcsr2.ensure((sizeof(int32_t) + sizeof(float)) * (size_t)std::max<int64_t>(nnz, 1) + 256, h->stream));
+            int32_t* col = (int32_t*)h->tcsr2.p;
+            float* val = (float*)(((uintptr_t)(col + nnz) + 255) & ~(uintptr_t)255);
+            CK(launch_dense_fill((const float*)Xd, n, h->dim, rp, col, val, h->stream));
+            CK(h->red.ensure(64, h->stream));
+            CK(launch_csr_check(rp, col, n, h->dim, (int*)h->red.p, h->stream));
+            int res[2] = {0, 0};
+            CK(cudaMemcpyAsync(res, h->red.p, sizeof(res), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            auto_csr = CsrIn{rp, col, val, res[1], nnz};
+            if (train_csr_supported(a.S, h->dim, res[1], h->max_smem_optin)) csr = &auto_csr;
+        }
+    }
     // CSR input: the sparse-distance kernel where W streams from global
     // memory; on-chip maps (latency-bound, no gain) and layouts it does not
     // cover train on the densified rows

@@ -34,10 +34,32 @@ def neuron_owner(u: int, world: int) -> tuple[int, int]:
     return u % world, u // world
 
 
+def broadcast_unique_id(rank: int, group=None, make_id=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL unique id (som_comm_unique_id) and
+    every rank receives it over torch.distributed (any backend)."""
+    import torch.distributed as dist
+
+    make_id = make_id or _som.som_comm_unique_id
+    obj = [make_id() if rank == 0 else None]
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def init_nccl(h, rank: int, world: int, shard_mode: int, group=None) -> None:
+    """Bind libsom's own NCCL communicator to handle h (som_comm_init_nccl):
+    SOM_SHARD_DOCS makes som_errors / som_errors_csr reduce their fp64 sum
+    and int64 counts over the ranks inside the library."""
+    uid = broadcast_unique_id(rank, group)
+    _som.som_comm_init_nccl(h, rank, world, uid, shard_mode)
+
+
 def reduce_errors(qe_local: float, te_local: float, n_local: int, group=None, device=None) -> tuple[float, float]:
-    """Global QE/TE from per-rank values over n_local documents each:
-    QE = sum_r qe_r n_r / sum_r n_r (qe_r n_r is the rank's fp64 sum of
-    sqrt(D1)); TE likewise from the integer counts."""
+    """Host-side model of the document-sharded error reduction, used by the
+    CPU (gloo) tests: QE = sum_r qe_r n_r / sum_r n_r (qe_r n_r is the rank's
+    fp64 sum of sqrt(D1)); TE likewise from the integer counts.  On GPUs the
+    library reduces the fp64 sums and int64 counts itself over NCCL
+    (init_nccl with SOM_SHARD_DOCS); this function is not on that path."""
     import torch
     import torch.distributed as dist
 
@@ -50,11 +72,12 @@ def reduce_errors(qe_local: float, te_local: float, n_local: int, group=None, de
 
 
 def errors_doc_sharded(m: "_som.SOM", X_shard, group=None, device=None) -> tuple[float, float]:
-    """QE and TE of the whole (document-sharded) corpus: each rank scores its
-    shard with som_errors on its GPU, then one 24-byte all-reduce."""
+    """QE and TE of the whole (document-sharded) corpus.  The handle must be
+    bound with init_nccl(..., SOM_SHARD_DOCS): som_errors then maps this
+    rank's shard and reduces the fp64 sum and int64 counts over NCCL inside
+    libsom (collective; an empty shard passes n = 0)."""
     n_local = int(X_shard.shape[0])
-    qe, te = (0.0, 0.0) if n_local == 0 else m.errors(X_shard)
-    return reduce_errors(qe, te, n_local, group=group, device=device)
+    return _som.som_errors(m.h, X_shard, n_local)
 
 
 def exchange_handles(blob: bytes, group=None) -> list[bytes]:
@@ -137,4 +160,5 @@ class ShardedSOM:
         barrier()
 
 
-__all__ = ["shard_range", "neuron_owner", "reduce_errors", "errors_doc_sharded", "exchange_handles", "ShardedSOM"]
+__all__ = ["shard_range", "neuron_owner", "broadcast_unique_id", "init_nccl", "reduce_errors", "errors_doc_sharded",
+           "exchange_handles", "ShardedSOM"]

@@ -50,7 +50,8 @@ EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights
            "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
            "som_last_stats", "som_last_error", "som_version", "som_comm_init", "som_comm_local_units",
            "som_comm_mailbox_ipc", "som_comm_set_peers_ipc", "som_comm_set_peers_dev", "som_comm_mailbox_ptr",
-           "som_comm_unique_id", "som_comm_init_nccl", "som_set_exchange"]
+           "som_comm_unique_id", "som_comm_init_nccl", "som_set_exchange", "som_init_random_csr", "som_fit",
+           "som_fit_csr", "som_last_phases"]
 
 
 def lib():
@@ -101,6 +102,10 @@ def lib():
         "som_comm_unique_id": [P],
         "som_comm_init_nccl": [P, i32, i32, P, i32],
         "som_set_exchange": [P, i32],
+        "som_init_random_csr": [P, P, P, P, i64, u64],
+        "som_fit": [P, P, i64, i32, f64, f64, P, u64, u64, P, P, P, P, P, P],
+        "som_fit_csr": [P, P, P, P, i64, i32, f64, f64, P, u64, u64, P, P, P, P, P, P],
+        "som_last_phases": [P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -432,6 +437,52 @@ def som_comm_init_nccl(h, rank: int, world: int, uid: bytes, shard_mode: int) ->
 
 def som_set_exchange(h, mode: int) -> None:
     _check(lib().som_set_exchange(h, mode))
+
+
+def som_init_random_csr(h, rowptr, col, val, n: int, seed: int) -> None:
+    _check_csr(rowptr, col, val, n)
+    _check(lib().som_init_random_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n,
+                                     seed & (2**64 - 1)))
+
+
+def _fit_outputs(h, n, bmu1, bmu2, d2, U):
+    for a, nm in ((bmu1, "bmu1"), (bmu2, "bmu2"), (d2, "d2")):
+        _need(a, n, nm)
+    d = _dims.get(_hv(h))
+    if d is not None:
+        _need(U, d[0], "U")
+
+
+def som_fit(h, X, n: int, epochs: int, alpha0: float, sigma0: float, sched: som_schedule | None, seed: int,
+            init_seed: int, bmu1=None, bmu2=None, d2=None, U=None) -> tuple[float, float]:
+    _check_rows(h, X, n)
+    _fit_outputs(h, n, bmu1, bmu2, d2, U)
+    q, t = ctypes.c_double(), ctypes.c_double()
+    sp = ctypes.byref(sched) if sched is not None else None
+    _check(lib().som_fit(h, _ptr(X, np.float32), n, epochs, alpha0, sigma0, sp, seed & (2**64 - 1),
+                         init_seed & (2**64 - 1), _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True),
+                         _ptr(d2, np.float32, True), ctypes.byref(q), ctypes.byref(t), _ptr(U, np.float32, True)))
+    return q.value, t.value
+
+
+def som_fit_csr(h, rowptr, col, val, n: int, epochs: int, alpha0: float, sigma0: float, sched: som_schedule | None,
+                seed: int, init_seed: int, bmu1=None, bmu2=None, d2=None, U=None) -> tuple[float, float]:
+    _check_csr(rowptr, col, val, n)
+    _fit_outputs(h, n, bmu1, bmu2, d2, U)
+    q, t = ctypes.c_double(), ctypes.c_double()
+    sp = ctypes.byref(sched) if sched is not None else None
+    _check(lib().som_fit_csr(h, _ptr(rowptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float32), n, epochs,
+                             alpha0, sigma0, sp, seed & (2**64 - 1), init_seed & (2**64 - 1),
+                             _ptr(bmu1, np.int32, True), _ptr(bmu2, np.int32, True), _ptr(d2, np.float32, True),
+                             ctypes.byref(q), ctypes.byref(t), _ptr(U, np.float32, True)))
+    return q.value, t.value
+
+
+def som_last_phases(h) -> tuple[list[float], float]:
+    ms = (ctypes.c_double * 5)()
+    tr = ctypes.c_double()
+    _check(lib().som_last_phases(h, ms, ctypes.byref(tr)))
+    return list(ms), tr.value
 
 
 def som_last_error() -> str:
