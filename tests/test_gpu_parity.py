@@ -263,9 +263,11 @@ def test_c2_full_schedule(som):
           f"bit-identical weights: {np.array_equal(W, Wo)}]", end="")
 
 
-def test_c3_prefix_global_kernel(som):
+def test_c3_prefix_global_kernel(som, monkeypatch):
     """c3 shape (50x50 hex, 10k terms; W = 100 MB streams from L2/HBM): the
-    pipelined global-memory kernel, first 150 steps, against the oracle."""
+    pipelined global-memory kernel (dense rows kept dense:
+    SOM_TRAIN_DENSE_CSR=0), first 150 steps, against the oracle."""
+    monkeypatch.setenv("SOM_TRAIN_DENSE_CSR", "0")
     C = bank_corpus(3000, 10000, seed=3)
     X = C.dense()
     W0 = init_rows(X, 2500, 1003)
