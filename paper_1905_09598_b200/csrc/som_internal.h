@@ -26,6 +26,7 @@ struct TrainArgs {
     int G;                     // grid size (co-resident CTAs)
     int xstride;               // slots per exchange parity: G rounded up to 32 (parities on separate lines)
     int poll_ns;               // back-off between exchange polls (0: spin)
+    unsigned long long spin_ns;   // exchange wait bound (globaltimer ns) before the abort
     int S;                     // max units per CTA = ceil(N / G)
     int64_t t0, t1;            // step range
     uint64_t seed;
@@ -67,7 +68,18 @@ struct TrainArgs {
 
 constexpr int kTracePhases = 8;
 constexpr int kMaxRanks = 8;
-constexpr unsigned kSpinLimitX = 1u << 24;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// bounded exchange spin: checked every 256 polls against %globaltimer
+struct Spin {
+    unsigned n = 0;
+    unsigned long long t0 = 0;
+};
 
 __device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -93,9 +105,11 @@ __device__ __forceinline__ void xchg_publish(const TrainArgs& a, unsigned long l
     if (lane == 0) st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.xstride + b, (key & ~0xFFull) | xchg_tag(t));
 }
 
-__device__ __forceinline__ bool xchg_should_stop(const TrainArgs& a, unsigned& spins, int lane) {
-    if ((++spins & 255u) != 0u) return false;
-    const bool s = spins > kSpinLimitX || ld_relaxed_u32(a.abort_flag) != 0u;
+__device__ __forceinline__ bool xchg_should_stop(const TrainArgs& a, Spin& spins, int lane) {
+    if ((++spins.n & 255u) != 0u) return false;
+    const unsigned long long now = globaltimer_ns();
+    if (spins.t0 == 0) spins.t0 = now;
+    const bool s = now - spins.t0 > a.spin_ns || ld_relaxed_u32(a.abort_flag) != 0u;
     if (__any_sync(0xffffffffu, s)) {
         if (lane == 0) atomicExch(a.abort_flag, 1u);
         return true;
@@ -107,7 +121,7 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
     const unsigned long long tag = xchg_tag(t);
     const unsigned long long* slots = a.xchg + (size_t)(t & 1) * a.xstride;
     unsigned long long gmin = 0;
-    unsigned spins = 0;
+    Spin spins;
     for (;;) {
         unsigned long long m = ~0ull;
         bool ok = true;
@@ -124,7 +138,7 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
     const size_t par = (size_t)(t & 1) * a.world;
     if (b == 0 && lane < a.world) st_relaxed_sys_u64(a.mail[lane] + par + a.rank, gmin);
     const unsigned long long* mine = a.mail[a.rank] + par;
-    spins = 0;
+    spins = Spin{};
     for (;;) {
         unsigned long long v = ~0ull;
         bool ok = true;
@@ -159,11 +173,6 @@ __device__ __forceinline__ int64_t train_row(const TrainArgs& a, int64_t t) {
 
 // global unit index of local unit l
 __device__ __forceinline__ int global_unit(const TrainArgs& a, int l) { return a.rank + a.world * l; }
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 // trace clock: %globaltimer (ns, comparable across SMs, coarse) or, with
 // SOM_TRACE_CLOCK=1, the SM cycle counter (fine, per-SM only)
 __device__ __forceinline__ unsigned long long trace_now(int clk) {

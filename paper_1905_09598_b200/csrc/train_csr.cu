@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
     __shared__ unsigned char upd[kMaxSlotsC];
     __shared__ int lst[kMaxSlotsC];            // [0, nup): slots of the pending update
     __shared__ int uid[kMaxSlotsC];            // local unit (W row) of slot s
-    __shared__ int s_nup, s_abort;
+    __shared__ int s_nup[2], s_abort;   // s_nup by step parity: no barrier A when a step updates nothing
     __shared__ long long nb[3][2];             // CSR bounds of x_t in nb[t % 3]
     __shared__ __align__(8) uint64_t mbar[8];
     extern __shared__ __align__(128) float sm[];
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
     for (int s = threadIdx.x; s < Sb; s += NT) uid[s] = a.utab ? a.utab[(size_t)b * a.S + s] : b + s * G;
     if (threadIdx.x == 0) {
         s_abort = 0;
-        s_nup = 0;
+        s_nup[a.t0 & 1] = 0;
         for (int r = 0; r < R_max; ++r) mbar_init_g(&mbar[r], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         bounds(a.t0);
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         if (a.trace && threadIdx.x == 0 && t - a.t0 < a.trace_steps)
             tr = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
         if (tr) tr[0] = trace_now(a.trace_clk);
-        const int nup = s_nup;
+        const int nup = s_nup[t & 1];
 
         // ---- dense pass over the pending update's rows (ring, issued by
         // thread 0 when the winner of t-1 was known)
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             }
             __syncwarp();
             if (lane == 0) {
-                s_nup = n_up;
+                s_nup[(t + 1) & 1] = n_up;
                 // first rows of the next pass into the ring (none after the
                 // last step: the final flush reads rows directly)
                 if (!stop && t + 1 < a.t1) {
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
 
     // flush the update of the last step (x_{t1-1} is now in xp)
     if (a.t1 > a.t0 && !s_abort) {
-        const int nup = s_nup;
+        const int nup = s_nup[a.t1 & 1];
         for (int i = 0; i < nup; ++i) {
             const int s = lst[i];
             const float h = hs[s];

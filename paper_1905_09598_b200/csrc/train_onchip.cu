@@ -481,6 +481,9 @@ __global__ void __launch_bounds__(NTH, 1) som_train_onchip_kernel(const TrainArg
                 }
             }
             tm_wait_st();
+            // streamed rows written back above are read again by the next
+            // step's ring prefill (async proxy): order the writes first
+            if (ng0 < nup) asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         q += nup - ng0;
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -644,8 +647,10 @@ bool train_onchip_plan(int S, int dim, int maxnnz, int max_smem_optin, int* ntm,
     int rmax = 2;
     if (const char* e = std::getenv("SOM_ONCHIP_RING")) rmax = std::max(1, std::min(4, std::atoi(e)));
     int best_s = 0, best_r = 0;
+    int smax = 8;   // SOM_ONCHIP_NSM caps the shared-memory rows (ring depth vs on-chip rows)
+    if (const char* e = std::getenv("SOM_ONCHIP_NSM")) smax = std::max(0, std::min(8, std::atoi(e)));
     // most on-chip rows first, then the deepest ring the rest of the budget allows
-    for (int s = std::min(S - t, 8); s >= 0; --s) {
+    for (int s = std::min(S - t, smax); s >= 0; --s) {
         const int rest = S - t - s;
         const int r = rest > 0 ? 1 : 0;
         if (fixed + (size_t)(s + r) * row <= budget) {

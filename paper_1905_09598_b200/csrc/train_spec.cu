@@ -56,7 +56,7 @@ __device__ __forceinline__ unsigned long long spec_wait(const TrainArgs& a, uint
     const unsigned long long* sa = spec_slot_a(a, q);
     const unsigned long long* sb = spec_slot_b(a, q);
     unsigned long long va[kSpecMaxG / 32], vb[kSpecMaxG / 32];
-    unsigned spins = 0;
+    Spin spins;
     for (;;) {
         bool ok = true;
 #pragma unroll
@@ -74,11 +74,11 @@ __device__ __forceinline__ unsigned long long spec_wait(const TrainArgs& a, uint
             }
         }
         if (__all_sync(0xffffffffu, ok)) break;
-        if (spins == 0 && tr) tr[5] = trace_now(a.trace_clk);
+        if (spins.n == 0 && tr) tr[5] = trace_now(a.trace_clk);
         if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
         if (a.poll_ns > 0) __nanosleep(a.poll_ns);
     }
-    if (tr) { tr[6] = trace_now(a.trace_clk); tr[4] = spins; }
+    if (tr) { tr[6] = trace_now(a.trace_clk); tr[4] = spins.n; }
     unsigned long long m = ~0ull;
 #pragma unroll
     for (int k = 0; k < kSpecMaxG / 32; ++k) m = umin64(m, va[k]);

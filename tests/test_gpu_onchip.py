@@ -17,6 +17,11 @@ pytestmark = pytest.mark.gpu
 KERNEL_ONCHIP = 9
 
 
+@pytest.fixture(autouse=True)
+def _onchip_on(monkeypatch):
+    monkeypatch.setenv("SOM_TRAIN_ONCHIP", "1")   # kernel 9 is opt-in
+
+
 @pytest.fixture(scope="module")
 def som():
     from paper_1905_09598_b200 import som as s
