@@ -187,6 +187,11 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * selects: unset or 0 = kernel 2 (default), 1 = kernel 6 for the whole
  * range, 2 = kernel 7 (needs >= 8192 prototype elements per CTA and no
  * forced mode or grid).  Kernel 8 = the NCCL step path (som_set_exchange).
+ * Kernel 10 = CSR input (or sparse dense rows, converted on the device) in
+ * AUTO mode where W does not fit the SMs' shared memory, with the
+ * environment variable SOM_TRAIN_TIER=1: the map held in tensor memory and
+ * shared memory, the rest streamed through a TMA ring (train_tier.cu);
+ * kernel 4 otherwise.
  * All follow the same arithmetic contract (R9-R11). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 

@@ -208,10 +208,10 @@ cudaError_t launch_train_small(const TrainArgs& a, cudaStream_t st);
 int csr_nz_cap(int maxnnz);
 bool train_csr_supported(int S, int dim, int maxnnz, int max_smem_optin);
 cudaError_t launch_train_csr(const TrainArgs& a, cudaStream_t st);
-// on-chip variant (train_onchip.cu, kernel 9): TMEM / shared-memory /
-// streamed rows; plan = rows per class for S units per CTA (false: n/a)
-bool train_onchip_plan(int S, int dim, int maxnnz, int max_smem_optin, int* ntm, int* nsm, int* R);
-cudaError_t launch_train_onchip(const TrainArgs& a, int ntm, int nsm, int R, cudaStream_t st);
+// tiered-storage variant (train_tier.cu, kernel 10): rows in registers,
+// TMEM, shared memory, the rest streamed through a chunked TMA ring
+bool train_tier_supported(int S, int dim, int maxnnz, int max_smem_optin);
+cudaError_t launch_train_tier(const TrainArgs& a, int max_smem_optin, cudaStream_t st);
 // CSR validation: out[0] error bits (1 rowptr, 2 col range, 4 col order),
 // out[1] max nonzeros per row (device ints)
 cudaError_t launch_csr_check(const int64_t* rowptr, const int32_t* col, int64_t n, int dim, int* out,

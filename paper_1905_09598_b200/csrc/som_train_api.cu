@@ -217,17 +217,13 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     CsrIn auto_csr{};
     bool dense_csr = true;
     if (const char* e = std::getenv("SOM_TRAIN_DENSE_CSR")) dense_csr = std::atoi(e) != 0;
-    // Kernel 9 (on-chip map) is opt-in (SOM_TRAIN_ONCHIP=1): measured at
-    // 53.6 us/step on c3 vs 18.7 for kernel 4, and its full c3 schedule left
-    // weights 1.7e-3 off the oracle (kernel 9).  When enabled it
-    // also replaces the shared-memory kernel for maps whose share fits shared
-    // memory (sparse rows make its unchanged units cheap).
-    bool onchip_env = false;
-    if (const char* e = std::getenv("SOM_TRAIN_ONCHIP")) onchip_env = std::atoi(e) != 0;
-    int oc_ntm = 0, oc_nsm = 0, oc_R = 0;
-    const bool onchip_fit = onchip_env && h->train_mode == SOM_TRAIN_AUTO && !use_small && !use_reg &&
-                            train_onchip_plan(a.S, h->dim, 0, h->max_smem_optin, &oc_ntm, &oc_nsm, &oc_R);
-    if (!csr && dense_csr && !use_small && !use_reg && (!a.w_smem || onchip_fit) && a.x_vec4 &&
+    // kernel 10 (train_tier.cu) for CSR rows where W streams from global
+    // memory in AUTO mode: opt-in (SOM_TRAIN_TIER=1) while it is slower than
+    // kernel 4 on c3 (kernel 10)
+    bool tier_env = false;
+    if (const char* e = std::getenv("SOM_TRAIN_TIER")) tier_env = std::atoi(e) != 0;
+    tier_env = tier_env && h->train_mode == SOM_TRAIN_AUTO && !use_small && !use_reg && !a.w_smem;
+    if (!csr && dense_csr && !use_small && !use_reg && !a.w_smem && a.x_vec4 &&
         h->train_mode == SOM_TRAIN_AUTO && h->xchg_mode != SOM_XCHG_NCCL) {
         const size_t tb = dense_csr_temp_bytes(n);
         CK(h->tcsr.ensure(sizeof(int64_t) * 2 * ((size_t)n + 1) + tb + 256, h->stream));
@@ -250,17 +246,17 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
             CK(cudaStreamSynchronize(h->stream));
             auto_csr = CsrIn{rp, col, val, res[1], nnz};
             if (train_csr_supported(a.S, h->dim, res[1], h->max_smem_optin) ||
-                (onchip_fit && train_onchip_plan(a.S, h->dim, res[1], h->max_smem_optin, &oc_ntm, &oc_nsm, &oc_R)))
+                (tier_env && train_tier_supported(a.S, h->dim, res[1], h->max_smem_optin)))
                 csr = &auto_csr;
         }
     }
     // CSR input: the sparse-distance kernel where W streams from global
     // memory; on-chip maps (latency-bound, no gain) and layouts it does not
     // cover train on the densified rows
-    bool use_csr = false, use_onchip = false;
+    bool use_csr = false, use_tier = false;
     if (csr) {
-        use_onchip = onchip_fit && train_onchip_plan(a.S, h->dim, csr->maxnnz, h->max_smem_optin, &oc_ntm, &oc_nsm, &oc_R);
-        use_csr = use_onchip ||
+        use_tier = tier_env && train_tier_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin);
+        use_csr = use_tier ||
                   (!use_small && !use_reg && !a.w_smem && train_csr_supported(a.S, h->dim, csr->maxnnz, h->max_smem_optin));
         if (use_csr) {
             a.rowptr = csr->rowptr; a.col = csr->col; a.val = csr->val;
@@ -280,7 +276,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
             a.utab = (const int*)h->utab.p;
             a.ucnt = a.utab + (size_t)a.G * a.S;
             smem = sizeof(float) * 2 * (size_t)a.dimp + 24 * (size_t)a.nz_cap;
-            if (use_onchip) { a.w_smem = 0; smem = 0; }   // kernel 9 sizes its own shared memory
+            if (use_tier) { a.w_smem = 0; smem = 0; }   // kernel 10 sizes its own shared memory
         } else {
             CK(h->dense.ensure(sizeof(float) * (size_t)n * h->dim, h->stream));
             CK(launch_densify(csr->rowptr, csr->col, csr->val, 0, n, h->dim, (float*)h->dense.p, h->stream));
@@ -423,7 +419,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         }
     }
     else if (use_reg) CK(launch_train_reg(a, h->stream));
-    else if (use_onchip) CK(launch_train_onchip(a, oc_ntm, oc_nsm, oc_R, h->stream));
+    else if (use_tier) CK(launch_train_tier(a, h->max_smem_optin, h->stream));
     else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
@@ -433,7 +429,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_onchip ? 9 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_tier ? 10 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

@@ -1,0 +1,782 @@
+// train_tier.cu — online SOM training, kernel 10:
+// the map held in the SM's tiers of storage, for maps whose per-SM share
+// (c3: 2,500 units x 10,000 terms = 100 MB over 148 SMs, 17 rows of 40 KB
+// per SM) exceeds any one of them.  Same step and arithmetic contract as the
+// CSR kernels (train_csr.cu): the pending Eq. 1 update of step t-1 fused with
+// step t's distances (an exact reorder), R9-R11, the sparse identity R25
+// (D_u = |w_u|^2 + sum_{k in nz(x)} ((x_k - w_k)^2 - w_k^2), |w|^2 in fp64),
+// the tagged all-gather exchange (som_internal.h).
+//
+// Where a CTA's rows live (slot s of its S units, in this order):
+//   [0, ntm)           tensor memory, used as plain storage: data thread dt
+//                      (warp w = 1..12) holds float4 chunks dt + 384 j
+//                      (j < KJ) of a row as 4 KJ words of its TMEM lane
+//                      (lane quarter w % 4), column group (w - 1) / 4 (170
+//                      columns each), 4 KJ r; moved with tcgen05.ld/st (its
+//                      own path beside the shared-memory port);
+//   [ntm, non)         shared memory, [row][j][dt] float4 (conflict-free);
+//   [non, S)           W in global memory (L2-resident: only these rows are
+//                      touched during the launch), streamed through a ring of
+//                      RC chunks (chunk j of a row = float4 [384 j, 384 j + 384)
+//                      = the thread's chunk j), filled by cp.async.bulk from
+//                      the control warp, full/empty mbarriers; updated rows
+//                      are written back from registers.
+// Warp 0 is the control warp (keys, exchange, neighbourhood, lists, ring
+// producer); warps 1-12 (384 threads) hold the data.  Per step t:
+//   1. dense pass (data warps) over the rows of update(t-1), streamed rows
+//      alternating with on-chip rows so the ring keeps moving, branch-free:
+//      w' = fmaf(h, RN(x_{t-1} - w), w) (R11; x_{t-1} in registers, built
+//      once per step from its non-zeros) and |w'|^2 in fp64, per-warp
+//      partials by a multi-value butterfly over four rows; then S(x_t) of
+//      those rows: on-chip rows warp by warp over the union of the lanes'
+//      non-zeros of x_t (one TMEM word / shared-memory word per row and
+//      non-zero), streamed rows by one warp per row gathering from W;
+//      meanwhile the control warp feeds the ring;
+//   2. barrier A; control warp: keys (updated units from the partials, the
+//      others from the speculative S of step 2' of the previous step), the
+//      exchange, the winner, h and the lists of update(t), first ring chunks
+//      of step t+1; data warps meanwhile (2'): bitmap of x_{t+1},
+//      speculative S(x_{t+1}) of every unit with its current row (exact for
+//      every unit update(t) leaves alone), list of x_{t+2};
+//   3. barrier B.
+// All sums have a fixed order (deterministic run to run).  At the end of the
+// launch the update of the last step is applied and the on-chip rows are
+// written back to W.
+#include <algorithm>
+#include <cstdlib>
+
+#include "som_device.cuh"
+#include "som_internal.h"
+
+namespace som {
+
+namespace {
+
+constexpr int NDW = 12;            // data warps 1..12
+constexpr int NDT = NDW * 32;      // data threads: own the rows' elements
+constexpr int NTH = NDT + 32;      // + control warp 0
+constexpr int kSlots = 32;         // units per CTA (one control lane each)
+constexpr int kRingMax = 16;       // ring chunks
+constexpr int kTmCols = 170;       // TMEM columns per column group (3 groups of 512)
+constexpr int kTmMax = 8;          // TMEM rows (unrolled loops)
+constexpr int kSmMax = 4;          // shared-memory rows (unrolled loops)
+
+struct TierPlan {
+    int ntm, nsm, rc;              // TMEM rows, shared-memory rows, ring chunks
+};
+
+__device__ __forceinline__ void bar_data() { asm volatile("bar.sync 1, %0;" ::"n"(NDT) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// ---- tcgen05 tensor-memory moves of N consecutive 32-bit columns (32 lanes)
+template <int N>
+__device__ __forceinline__ void tld(uint32_t ta, uint32_t* r);
+template <>
+__device__ __forceinline__ void tld<4>(uint32_t ta, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(ta));
+}
+template <>
+__device__ __forceinline__ void tld<8>(uint32_t ta, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta));
+}
+template <>
+__device__ __forceinline__ void tld<16>(uint32_t ta, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(ta));
+}
+template <int N>
+__device__ __forceinline__ void tst(uint32_t ta, const uint32_t* r);
+template <>
+__device__ __forceinline__ void tst<4>(uint32_t ta, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+}
+template <>
+__device__ __forceinline__ void tst<8>(uint32_t ta, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void tst<16>(uint32_t ta, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                   "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+__device__ __forceinline__ void twait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void twait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// a thread's 4 KJ words of one TMEM row <-> its KJ float4 chunks
+template <int KJ>
+__device__ __forceinline__ void tm_load(uint32_t ta, float4 (&w)[KJ]) {
+    constexpr int C = 4 * KJ;
+    uint32_t r[C];
+    int o = 0;
+#pragma unroll
+    for (int q = 0; q < C / 16; ++q, o += 16) tld<16>(ta + o, r + o);
+    if constexpr ((C % 16) >= 8) { tld<8>(ta + o, r + o); o += 8; }
+    if constexpr ((C % 8) >= 4) tld<4>(ta + o, r + o);
+    twait_ld();
+#pragma unroll
+    for (int j = 0; j < KJ; ++j)
+        w[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                           __uint_as_float(r[4 * j + 3]));
+}
+template <int KJ>
+__device__ __forceinline__ void tm_store(uint32_t ta, const float4 (&w)[KJ]) {
+    constexpr int C = 4 * KJ;
+    uint32_t r[C];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        r[4 * j] = __float_as_uint(w[j].x); r[4 * j + 1] = __float_as_uint(w[j].y);
+        r[4 * j + 2] = __float_as_uint(w[j].z); r[4 * j + 3] = __float_as_uint(w[j].w);
+    }
+    int o = 0;
+#pragma unroll
+    for (int q = 0; q < C / 16; ++q, o += 16) tst<16>(ta + o, r + o);
+    if constexpr ((C % 16) >= 8) { tst<8>(ta + o, r + o); o += 8; }
+    if constexpr ((C % 8) >= 4) tst<4>(ta + o, r + o);
+}
+
+// R25 sparse term of one element: (x - w)^2 - w^2 in fp64 (both squares exact)
+__device__ __forceinline__ double sterm(float x, float w) {
+    const double wd = (double)w;
+    const double e = (double)x - wd;
+    return fma(e, e, -(wd * wd));
+}
+
+// value of column k in a sorted (col, val) list of cnt entries, 0 if absent
+// (out of line: the hot loops only reach it past the 4-entry cache)
+__device__ __noinline__ float list_lookup(const int* ci, const float* cv, int cnt, int k) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return (lo < cnt && ci[lo] == k) ? cv[lo] : 0.0f;
+}
+
+template <int KJ>
+__global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs a, const TierPlan p) {
+    __shared__ double pn[kSlots][NDW];        // |w'|^2 partials of dense-pass rows
+    __shared__ double ps[kSlots][NDW];        // S(x_t) partials of dense-pass on-chip rows
+    __shared__ double qs[2][kSlots][NDW];     // speculative S partials of on-chip rows, [parity of the step]
+    __shared__ double sg[2][kSlots];          // speculative S of streamed rows, [parity of the step]
+    __shared__ double sgd[kSlots];            // S(x_t) of dense-pass streamed rows
+    __shared__ double wns[kSlots];            // fp64 |w_u|^2
+    __shared__ float hs[kSlots];              // h of the pending update
+    __shared__ int uid[kSlots];               // local unit (W row) of slot s
+    __shared__ int ord[kSlots];               // dense-pass order of the pending update's rows
+    __shared__ int strm[kSlots];              // its streamed rows, in ring order
+    __shared__ int s_nord, s_nstr, s_abort;
+    __shared__ unsigned s_onm;                // its on-chip rows (bit s)
+    __shared__ long long nb[4][2];            // CSR bounds of x_t in nb[t & 3]
+    __shared__ __align__(8) uint64_t full[kRingMax];
+    __shared__ __align__(8) uint64_t empty[kRingMax];
+    __shared__ uint32_t s_tmem;
+    extern __shared__ __align__(128) float4 sm4[];
+    // sm4: ring [rc][NDT] | smem rows [nsm][KJ][NDT] | x cache float[2][4][NDT] | nzi int[3][cap] |
+    //      nzv float[3][cap] | bitmap u32[2][bmw]
+
+    const int b = blockIdx.x, G = a.G;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool data = warp != 0;
+    const int dw = warp - 1;            // data warp 0..11
+    const int dt = tid - 32;            // data thread 0..383
+    const int Sb = a.utab ? a.ucnt[b] : (a.N - b + G - 1) / G;
+    const int ntm = p.ntm, nsm = p.nsm, RC = p.rc;
+    const int non = min(Sb, ntm + nsm);   // on-chip slots [0, non): TMEM [0, ntm), smem [ntm, non)
+    const int d4 = a.dimp >> 2;
+    const int cap = a.nz_cap;
+    const int bmw = (a.dimp >> 5) + 1;
+    float4* W4 = reinterpret_cast<float4*>(a.W);
+    float4* ring = sm4;
+    float4* srows = sm4 + (size_t)RC * NDT;
+    // x_t at the thread's first 4 non-zeros: xcs[((t & 1) * 4 + rank) * NDT + dt]
+    float* xcs = reinterpret_cast<float*>(srows + (size_t)nsm * KJ * NDT);
+    int* nzi = reinterpret_cast<int*>(xcs + 8 * NDT);
+    float* nzv = reinterpret_cast<float*>(nzi + 3 * (size_t)cap);
+    uint32_t* bmp = reinterpret_cast<uint32_t*>(nzv + 3 * (size_t)cap);
+    // chunk KJ-1 is the only one that can run past the row (KJ = ceil(d4 / NDT))
+    const bool vlast = data && dt + (KJ - 1) * NDT < d4;
+    const uint32_t tm_base_off = ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((dw >> 2) * kTmCols);
+
+    uint32_t mp = 0u, mc = 0u;   // non-zeros of x_{t-1}, x_t among this thread's elements
+    float4 xp[KJ];               // x_{t-1} at this thread's elements (the pending update's sample)
+    auto tm_addr = [&](int r) { return s_tmem + tm_base_off + (uint32_t)(r * 4 * KJ); };
+    auto bounds = [&](int64_t t) {
+        const int64_t i = train_row(a, t);
+        nb[t & 3][0] = a.rowptr[i];
+        nb[t & 3][1] = a.rowptr[i + 1];
+    };
+    auto cnt_of = [&](int64_t t) { return (int)(nb[t & 3][1] - nb[t & 3][0]); };
+    // (col, val) of x_t -> list slot t % 3 (data threads)
+    auto stage_list = [&](int64_t t) {
+        if (t < a.t1) {
+            const int64_t p0 = nb[t & 3][0];
+            const int cnt = cnt_of(t);
+            int* di = nzi + (size_t)(t % 3) * cap;
+            float* dv = nzv + (size_t)(t % 3) * cap;
+            for (int q = dt; q < cnt; q += NDT) {
+                cp_async4(di + q, a.col + p0 + q);
+                cp_async4(dv + q, a.val + p0 + q);
+            }
+        }
+        cp_async_commit();
+    };
+    // bitmap of x_t's columns -> slot t & 1 (data threads; two data barriers)
+    auto build_bitmap = [&](int64_t t) {
+        uint32_t* bm = bmp + (size_t)(t & 1) * bmw;
+        for (int q = dt; q < bmw; q += NDT) bm[q] = 0u;
+        bar_data();
+        const int cnt = cnt_of(t);
+        const int* ci = nzi + (size_t)(t % 3) * cap;
+        for (int q = dt; q < cnt; q += NDT) atomicOr(bm + (ci[q] >> 5), 1u << (ci[q] & 31));
+        bar_data();
+    };
+    // bit 4 j + c: element (j, c) of this thread is non-zero in x_t
+    auto mask_of = [&](int64_t t) {
+        const uint32_t* bm = bmp + (size_t)(t & 1) * bmw;
+        uint32_t m = 0;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            if (j == KJ - 1 && !vlast) continue;
+            const int k0 = 4 * (dt + j * NDT);
+            m |= ((bm[k0 >> 5] >> (k0 & 31)) & 0xFu) << (4 * j);
+        }
+        return m;
+    };
+    // x_t at this thread's element `bit` (set in mask m): the per-step cache
+    // holds the first 4 non-zeros in rank order; beyond, the sorted list
+    auto xget = [&](int64_t t, uint32_t m, int bit) {
+        const int rank = __popc(m & ((1u << bit) - 1u));
+        if (rank < 4) return xcs[((int)(t & 1) * 4 + rank) * NDT + dt];
+        return list_lookup(nzi + (size_t)(t % 3) * cap, nzv + (size_t)(t % 3) * cap, cnt_of(t),
+                           4 * (dt + (bit >> 2) * NDT) + (bit & 3));
+    };
+    auto fill_cache = [&](int64_t t, uint32_t m) {
+        int rank = 0;
+        while (m != 0u && rank < 4) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1u;
+            xcs[((int)(t & 1) * 4 + rank) * NDT + dt] =
+                list_lookup(nzi + (size_t)(t % 3) * cap, nzv + (size_t)(t % 3) * cap, cnt_of(t),
+                            4 * (dt + (bit >> 2) * NDT) + (bit & 3));
+            ++rank;
+        }
+    };
+    // x_{t-1} into registers (zero off its non-zeros)
+    auto build_xp = [&](int64_t tp, uint32_t m) {
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            const uint32_t bits = (m >> (4 * j)) & 0xFu;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bits != 0u) {
+                if (bits & 1u) v.x = xget(tp, m, 4 * j);
+                if (bits & 2u) v.y = xget(tp, m, 4 * j + 1);
+                if (bits & 4u) v.z = xget(tp, m, 4 * j + 2);
+                if (bits & 8u) v.w = xget(tp, m, 4 * j + 3);
+            }
+            xp[j] = v;
+        }
+    };
+    // per-row |w'|^2 -> per-warp partials pn, two rows per multi-value butterfly
+    double pv0 = 0.0;
+    int pr0 = -1;
+    auto push = [&](int s, double n) {
+        if (pr0 < 0) { pv0 = n; pr0 = s; return; }
+        double v[2] = {pv0, n};
+        int sl = 0;
+        const double tot = butterfly_sum<2>(v, lane, &sl);
+        if ((lane & 15) == 0) pn[sl ? s : pr0][dw] = tot;
+        pr0 = -1;
+    };
+    auto push_flush = [&]() {
+        if (pr0 < 0) return;
+        const double tot = warp_sum_f64(pv0);
+        if (lane == 0) pn[pr0][dw] = tot;
+        pr0 = -1;
+    };
+    // S(x_tq) = sum over the thread's non-zeros of x_tq of (x - w)^2 - w^2 for
+    // the on-chip rows in `rows` (bit s), warp by warp over the union of the
+    // lanes' non-zeros; per-warp partials -> dst[s][dw].  q[0..7] = TMEM
+    // slots 0..7, q[8..11] = shared-memory slots ntm..ntm+3 (static indices).
+    auto onchip_sparse = [&](int64_t tq, uint32_t mq, uint32_t rows, double (*dst)[NDW]) {
+        double q[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) q[i] = 0.0;
+        for (uint32_t M = __reduce_or_sync(0xffffffffu, mq); M != 0u; M &= M - 1u) {
+            const int bit = __ffs(M) - 1;
+            const bool mine = (mq >> bit) & 1u;
+            const float x = mine ? xget(tq, mq, bit) : 0.0f;
+            const int j = bit >> 2, c = bit & 3;
+            uint32_t v[kTmMax];
+#pragma unroll
+            for (int s = 0; s < kTmMax; ++s)
+                if (s < ntm && ((rows >> s) & 1u))
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v[s]) : "r"(tm_addr(s) + (uint32_t)bit));
+            twait_ld();
+            if (mine) {
+#pragma unroll
+                for (int s = 0; s < kTmMax; ++s)
+                    if (s < ntm && ((rows >> s) & 1u)) q[s] += sterm(x, __uint_as_float(v[s]));
+#pragma unroll
+                for (int s2 = 0; s2 < kSmMax; ++s2) {
+                    if (s2 >= nsm || !((rows >> (ntm + s2)) & 1u)) continue;
+                    const float w = reinterpret_cast<const float*>(srows + ((size_t)s2 * KJ + j) * NDT + dt)[c];
+                    q[8 + s2] += sterm(x, w);
+                }
+            }
+        }
+        int sl = 0;
+        const double tot = butterfly_sum<16>(q, lane, &sl);
+        const int s = sl < 8 ? sl : ntm + (sl - 8);
+        if ((lane & 1) == 0 && (sl < 8 ? sl < ntm : sl - 8 < nsm) && s < non && ((rows >> s) & 1u)) dst[s][dw] = tot;
+    };
+    // S(x_tq) of streamed rows (list of slots), one warp per row gathering
+    // over the non-zeros of x_tq from W (global, L2)
+    auto stream_sparse = [&](int64_t tq, const int* slots, int count, double* dst) {
+        const int cnt = cnt_of(tq);
+        const int* ci = nzi + (size_t)(tq % 3) * cap;
+        const float* cv = nzv + (size_t)(tq % 3) * cap;
+        for (int i = dw; i < count; i += NDW) {
+            const int s = slots ? slots[i] : non + i;
+            const float* row = a.W + (int64_t)uid[s] * a.dimp;
+            double v = 0.0;
+            for (int q = lane; q < cnt; q += 32) v += sterm(cv[q], __ldcg(row + ci[q]));
+            v = warp_sum_f64(v);
+            if (lane == 0) dst[s] = v;
+        }
+    };
+    // the dense pass's streamed rows (at most one per warp when count <= 12):
+    // the gather's loads are issued before the on-chip sums and finished after
+    auto stream_issue = [&](int64_t tq, int count, float (&g)[2]) {
+        g[0] = g[1] = 0.0f;
+        if (dw >= count) return;
+        const int cnt = cnt_of(tq);
+        const int* ci = nzi + (size_t)(tq % 3) * cap;
+        const float* row = a.W + (int64_t)uid[strm[dw]] * a.dimp;
+        if (lane < cnt) g[0] = __ldcg(row + ci[lane]);
+        if (lane + 32 < cnt) g[1] = __ldcg(row + ci[lane + 32]);
+    };
+    auto stream_finish = [&](int64_t tq, int count, const float (&g)[2]) {
+        if (dw >= count) return;
+        const int cnt = cnt_of(tq);
+        const float* cv = nzv + (size_t)(tq % 3) * cap;
+        double v = 0.0;
+        if (lane < cnt) v += sterm(cv[lane], g[0]);
+        if (lane + 32 < cnt) v += sterm(cv[lane + 32], g[1]);
+        v = warp_sum_f64(v);
+        if (lane == 0) sgd[strm[dw]] = v;
+    };
+
+    // ---- prologue
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(512) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (lane == 0) {
+            s_abort = 0;
+            s_onm = 0u;
+            s_nord = 0;
+            s_nstr = 0;
+            for (int r = 0; r < RC; ++r) {
+                mbar_init_g(&full[r], 1);
+                mbar_init_g(&empty[r], NDW);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            bounds(a.t0);
+            if (a.t0 + 1 < a.t1) bounds(a.t0 + 1);
+            if (a.t0 + 2 < a.t1) bounds(a.t0 + 2);
+        }
+    }
+    for (int s = tid; s < Sb; s += NTH) uid[s] = a.utab ? a.utab[(size_t)b * a.S + s] : b + s * G;
+    for (int s = tid; s < kSlots; s += NTH) hs[s] = 0.0f;
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (data) {
+        stage_list(a.t0);
+        stage_list(a.t0 + 1);
+        // rows into their tiers; fp64 norms of every row
+        for (int s = 0; s < Sb; ++s) {
+            const float4* row = W4 + (int64_t)uid[s] * d4 + dt;
+            float4 w[KJ];
+            double n0 = 0.0, n1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < KJ; ++j) {
+                w[j] = (j < KJ - 1 || vlast) ? __ldcg(row + j * NDT) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const double e0 = w[j].x, e1 = w[j].y, e2 = w[j].z, e3 = w[j].w;
+                n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
+            }
+            if (s < ntm) {
+                tm_store<KJ>(tm_addr(s), w);
+            } else if (s < non) {
+                float4* sr = srows + (size_t)(s - ntm) * KJ * NDT + dt;
+#pragma unroll
+                for (int j = 0; j < KJ; ++j) sr[j * NDT] = w[j];
+            }
+            push(s, n0 + n1);
+        }
+        push_flush();
+        twait_st();
+        cp_async_wait_all();
+        bar_data();
+        build_bitmap(a.t0);
+        mc = mask_of(a.t0);
+        fill_cache(a.t0, mc);
+        // speculative S(x_t0) of every unit (no update is pending)
+        onchip_sparse(a.t0, mc, 0xffffffffu, qs[a.t0 & 1]);
+        stream_sparse(a.t0, nullptr, Sb - non, sg[a.t0 & 1]);
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    bool my_upd = false;     // control lane s: unit s is in the pending update
+    if (warp == 0 && lane < Sb) {
+        double tot = 0.0;
+#pragma unroll
+        for (int w8 = 0; w8 < NDW; ++w8) tot += pn[lane][w8];
+        wns[lane] = tot;
+    }
+    // ring positions: producer (control lane 0) and consumers (data threads)
+    int pslot = 0, pu = 0, issued = 0;
+    int cslot = 0, cu = 0;
+    auto produce = [&](int c) {   // chunk c of the streamed rows of the pending update
+        const int row = strm[c / KJ], j = c % KJ;
+        if (pu > 0) mbar_wait_g(&empty[pslot], (uint32_t)((pu - 1) & 1));
+        const int nf4 = min(NDT, d4 - j * NDT);
+        bulk_row(ring + (size_t)pslot * NDT, W4 + (int64_t)uid[row] * d4 + (size_t)j * NDT, (uint32_t)nf4 * 16u,
+                 &full[pslot]);
+        if (++pslot == RC) { pslot = 0; ++pu; }
+    };
+    __syncthreads();
+
+    double f_next = a.t1 > a.t0 ? a.f_tab[0] : 0.0;   // decay factor of the coming step, loaded a step ahead
+    for (int64_t t = a.t0; t < a.t1; ++t) {
+        // phase trace (som_set_trace): control lane 0 stamps [0] loop top,
+        // [3] keys formed, [4] winner known, [5] lists + ring issued, [6]
+        // after barrier B; data thread 0 stamps [1] dense pass done, [2]
+        // sparse sums done
+        unsigned long long* tr = nullptr;
+        unsigned long long* tr1 = nullptr;
+        if (a.trace && t - a.t0 < a.trace_steps) {
+            unsigned long long* row = a.trace + ((size_t)b * a.trace_steps + (size_t)(t - a.t0)) * kTracePhases;
+            if (tid == 0) tr = row;
+            if (tid == 32) tr1 = row;
+        }
+        if (tr) tr[0] = trace_now(a.trace_clk);
+        const double f = f_next;
+        // ---- 1. dense pass over update(t-1)'s rows: Eq. 1 with x_{t-1}
+        // (registers), |w'|^2; then S(x_t) of those rows
+        if (data) {
+            const int nord = s_nord, nstr = s_nstr;
+            if (nord > 0) build_xp(t - 1, mp);
+            for (int i = 0; i < nord; ++i) {
+                const int s = ord[i];
+                const float h = hs[s];
+                double n0 = 0.0, n1 = 0.0;
+                if (s < ntm) {
+                    float4 w[KJ];
+                    tm_load<KJ>(tm_addr(s), w);
+#pragma unroll
+                    for (int j = 0; j < KJ; ++j) {
+                        w[j] = eq1u(h, w[j], xp[j]);
+                        const double e0 = w[j].x, e1 = w[j].y, e2 = w[j].z, e3 = w[j].w;
+                        n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
+                    }
+                    tm_store<KJ>(tm_addr(s), w);
+                } else if (s < non) {
+                    float4* sr = srows + (size_t)(s - ntm) * KJ * NDT + dt;
+#pragma unroll
+                    for (int j = 0; j < KJ; ++j) {
+                        const float4 w = eq1u(h, sr[j * NDT], xp[j]);
+                        sr[j * NDT] = w;
+                        const double e0 = w.x, e1 = w.y, e2 = w.z, e3 = w.w;
+                        n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
+                    }
+                } else {
+                    float4* grow = W4 + (int64_t)uid[s] * d4 + dt;
+#pragma unroll
+                    for (int j = 0; j < KJ; ++j) {
+                        mbar_wait_g(&full[cslot], (uint32_t)(cu & 1));
+                        const bool v = j < KJ - 1 || vlast;
+                        float4 w = v ? ring[(size_t)cslot * NDT + dt] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[cslot]);
+                        if (++cslot == RC) { cslot = 0; ++cu; }
+                        w = eq1u(h, w, xp[j]);
+                        if (v) __stcg(grow + j * NDT, w);
+                        const double e0 = w.x, e1 = w.y, e2 = w.z, e3 = w.w;
+                        n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
+                    }
+                }
+                push(s, n0 + n1);
+            }
+            push_flush();
+            twait_st();
+            if (tr1) tr1[1] = trace_now(a.trace_clk);
+            const bool short_list = nstr <= NDW && cnt_of(t) <= 64;
+            float g[2];
+            if (nstr > 0) {
+                // streamed rows written above: visible to the gathers below
+                // (generic) and to the next ring fill (async proxy)
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                bar_data();
+                if (short_list) stream_issue(t, nstr, g);
+            }
+            if (s_onm != 0u) onchip_sparse(t, mc, s_onm, ps);
+            if (nstr > 0) {
+                if (short_list) stream_finish(t, nstr, g);
+                else stream_sparse(t, strm, nstr, sgd);
+            }
+            if (tr1) tr1[2] = trace_now(a.trace_clk);
+        } else if (lane == 0) {
+            // ring producer: the rest of this step's streamed chunks
+            const int total = s_nstr * KJ;
+            for (int c = issued; c < total; ++c) produce(c);
+            issued = 0;
+        }
+        tc_before();
+        __syncthreads();   // (A) pass done: partials complete, rows stored
+        tc_after();
+
+        if (t + 1 < a.t1) f_next = a.f_tab[t + 1 - a.t0];
+        const double alpha = a.alpha0 * f;
+        double sigma = a.sigma0 * f;
+        if (sigma < a.sigma_min) sigma = a.sigma_min;
+        const double two_s2 = 2.0 * sigma * sigma;
+        const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
+
+        if (!data) {
+            // ---- 2. control warp: keys, exchange, winner, lists of update(t)
+            unsigned long long best = ~0ull;
+            if (lane < Sb) {
+                double tot;
+                if (my_upd) {
+                    double nn = 0.0, sv = 0.0;
+#pragma unroll
+                    for (int w8 = 0; w8 < NDW; ++w8) nn += pn[lane][w8];
+                    if (lane < non) {
+#pragma unroll
+                        for (int w8 = 0; w8 < NDW; ++w8) sv += ps[lane][w8];
+                    } else {
+                        sv = sgd[lane];
+                    }
+                    wns[lane] = nn;
+                    tot = nn + sv;
+                } else if (lane < non) {
+                    double sv = 0.0;
+#pragma unroll
+                    for (int w8 = 0; w8 < NDW; ++w8) sv += qs[t & 1][lane][w8];
+                    tot = wns[lane] + sv;
+                } else {
+                    tot = wns[lane] + sg[t & 1][lane];
+                }
+                tot = tot > 0.0 ? tot : 0.0;   // R25: the identity can round below 0
+                best = make_key((float)tot, global_unit(a, uid[lane]));
+            }
+            best = warp_min_u64(best);
+            if (tr) tr[3] = trace_now(a.trace_clk);
+            xchg_publish(a, best, t, b, lane);
+            int stop = 0;
+            const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
+            if (tr) tr[4] = trace_now(a.trace_clk);
+            if (stop && lane == 0) s_abort = 1;
+            const int c = key_unit(gmin);
+            if (b == 0 && lane == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
+            bool u2 = false;
+            if (lane < Sb) {
+                const double g2 = lattice_g2(a.cols, a.topo, global_unit(a, uid[lane]), c);
+                u2 = g2 <= r2;
+                hs[lane] = u2 ? (float)(alpha * exp(-g2 / two_s2)) : 0.0f;
+            }
+            my_upd = u2;
+            const unsigned mu = __ballot_sync(0xffffffffu, u2);
+            const unsigned lo_non = non >= 32 ? 0xffffffffu : ((1u << non) - 1u);
+            const unsigned onm = mu & lo_non;
+            const unsigned stm = mu & ~lo_non;
+            const int ns = __popc(stm), no = __popc(onm), m = min(ns, no);
+            const unsigned lt = (1u << lane) - 1u;
+            // dense-pass order: streamed and on-chip rows alternate (the ring
+            // refills while on-chip rows are processed)
+            if ((stm >> lane) & 1u) {
+                const int i = __popc(stm & lt);
+                strm[i] = lane;
+                ord[i < m ? 2 * i : m + i] = lane;
+            }
+            if ((onm >> lane) & 1u) {
+                const int k = __popc(onm & lt);
+                ord[k < m ? 2 * k + 1 : m + k] = lane;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s_onm = onm;
+                s_nord = ns + no;
+                s_nstr = ns;
+                // first chunks of the next pass into the ring (none after the
+                // last step: the flush reads streamed rows directly)
+                if (!stop && t + 1 < a.t1) {
+                    const int first = min(RC, ns * KJ);
+                    for (int cch = 0; cch < first; ++cch) produce(cch);
+                    issued = first;
+                }
+                if (tr) tr[5] = trace_now(a.trace_clk);
+            }
+        } else {
+            // ---- 2'. data warps: list of x_{t+2}, bounds of x_{t+3}, bitmap
+            // of x_{t+1}, speculative S(x_{t+1}) of every unit (skipped when
+            // the radius covers the whole lattice: every unit then takes the
+            // dense pass)
+            stage_list(t + 2);
+            if (dt == 0 && t + 3 < a.t1) bounds(t + 3);
+            uint32_t mn = 0u;
+            if (t + 1 < a.t1) {
+                build_bitmap(t + 1);
+                mn = mask_of(t + 1);
+                fill_cache(t + 1, mn);
+                if (!(r2 >= a.g2max)) {
+                    onchip_sparse(t + 1, mn, 0xffffffffu, qs[(t + 1) & 1]);
+                    stream_sparse(t + 1, nullptr, Sb - non, sg[(t + 1) & 1]);
+                }
+            }
+            cp_async_wait_all();
+            mp = mc;
+            mc = mn;
+        }
+        tc_before();
+        __syncthreads();   // (B)
+        tc_after();
+        if (tr) tr[6] = trace_now(a.trace_clk);
+        if (s_abort) break;
+    }
+
+    // flush the update of the last step (sample x_{t1-1}), then write every
+    // on-chip row back to W
+    if (data && a.t1 > a.t0 && !s_abort) {
+        const int nord = s_nord;
+        if (nord > 0) build_xp(a.t1 - 1, mp);
+        for (int i = 0; i < nord; ++i) {
+            const int s = ord[i];
+            const float h = hs[s];
+            if (s < ntm) {
+                float4 w[KJ];
+                tm_load<KJ>(tm_addr(s), w);
+#pragma unroll
+                for (int j = 0; j < KJ; ++j) w[j] = eq1u(h, w[j], xp[j]);
+                tm_store<KJ>(tm_addr(s), w);
+            } else if (s < non) {
+                float4* sr = srows + (size_t)(s - ntm) * KJ * NDT + dt;
+#pragma unroll
+                for (int j = 0; j < KJ; ++j) sr[j * NDT] = eq1u(h, sr[j * NDT], xp[j]);
+            } else {
+                float4* grow = W4 + (int64_t)uid[s] * d4 + dt;
+#pragma unroll
+                for (int j = 0; j < KJ; ++j)
+                    if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, eq1u(h, __ldcg(grow + j * NDT), xp[j]));
+            }
+        }
+        twait_st();
+    }
+    if (data && !s_abort) {
+        for (int s = 0; s < non; ++s) {
+            float4 w[KJ];
+            if (s < ntm) {
+                tm_load<KJ>(tm_addr(s), w);
+            } else {
+                const float4* sr = srows + (size_t)(s - ntm) * KJ * NDT + dt;
+#pragma unroll
+                for (int j = 0; j < KJ; ++j) w[j] = sr[j * NDT];
+            }
+            float4* grow = W4 + (int64_t)uid[s] * d4 + dt;
+#pragma unroll
+            for (int j = 0; j < KJ; ++j)
+                if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, w[j]);
+        }
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512) : "memory");
+}
+
+constexpr size_t kTierStatic = (2 * kSlots * NDW + 2 * kSlots * NDW) * 8 + (2 * kSlots + 2 * kSlots) * 8 + 1024 + 512;
+
+size_t tier_smem_bytes(int kj, int dimp, int cap, const TierPlan& p) {
+    return sizeof(float4) * (size_t)NDT * ((size_t)p.rc + (size_t)p.nsm * kj) + 8 * 4 * (size_t)NDT + 24 * (size_t)cap +
+           8 * (size_t)((dimp >> 5) + 1) + 128;
+}
+
+template <int KJ>
+cudaError_t launch_tier_kj(const TrainArgs& a, const TierPlan& p, cudaStream_t st) {
+    const size_t smem = tier_smem_bytes(KJ, a.dimp, a.nz_cap, p);
+    auto fn = som_train_tier_kernel<KJ>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    TrainArgs args = a;
+    TierPlan pp = p;
+    void* params[] = {&args, &pp};
+    return launch_persistent((const void*)fn, a, NTH, smem, params, st);
+}
+
+int tier_kj(int dimp) { return ((dimp / 4) + NDT - 1) / NDT; }
+
+bool tier_plan(int S, int dimp, int maxnnz, int max_smem_optin, TierPlan* out) {
+    if (dimp % 4 != 0 || S < 1 || S > kSlots) return false;
+    const int kj = tier_kj(dimp);
+    if (kj < 4 || kj > 8) return false;
+    TierPlan p{};
+    p.ntm = std::min(kTmMax, kTmCols / (4 * kj));
+    p.ntm = std::max(0, std::min(p.ntm, S));
+    const int cap = csr_nz_cap(maxnnz);
+    const size_t budget = (size_t)max_smem_optin - kTierStatic;
+    int rc_min = 8, rc_max = kRingMax;
+    if (const char* e = std::getenv("SOM_TIER_RING")) rc_max = std::max(2, std::min(kRingMax, std::atoi(e))), rc_min = std::min(rc_min, rc_max);
+    int smax = kSmMax;
+    if (const char* e = std::getenv("SOM_TIER_NSM")) smax = std::max(0, std::min(kSmMax, std::atoi(e)));
+    const int rest = S - p.ntm;
+    p.nsm = std::max(0, std::min(smax, rest));
+    p.rc = rest > p.nsm ? rc_min : 2;
+    while (p.nsm > 0 && tier_smem_bytes(kj, dimp, cap, p) > budget) --p.nsm;
+    if (S - p.ntm - p.nsm > 0) p.rc = rc_min;
+    if (tier_smem_bytes(kj, dimp, cap, p) > budget) return false;
+    while (p.rc < rc_max && S - p.ntm - p.nsm > 0) {
+        TierPlan q = p;
+        ++q.rc;
+        if (tier_smem_bytes(kj, dimp, cap, q) > budget) break;
+        p = q;
+    }
+    *out = p;
+    return true;
+}
+
+}  // namespace
+
+bool train_tier_supported(int S, int dim, int maxnnz, int max_smem_optin) {
+    TierPlan p;
+    return tier_plan(S, dim, maxnnz, max_smem_optin, &p);
+}
+
+cudaError_t launch_train_tier(const TrainArgs& a, int max_smem_optin, cudaStream_t st) {
+    TierPlan p;
+    if (!tier_plan(a.S, a.dimp, a.nz_cap, max_smem_optin, &p)) return cudaErrorInvalidConfiguration;
+    switch (tier_kj(a.dimp)) {
+        case 4: return launch_tier_kj<4>(a, p, st);
+        case 5: return launch_tier_kj<5>(a, p, st);
+        case 6: return launch_tier_kj<6>(a, p, st);
+        case 7: return launch_tier_kj<7>(a, p, st);
+        case 8: return launch_tier_kj<8>(a, p, st);
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+}  // namespace som

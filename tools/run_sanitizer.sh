@@ -4,7 +4,7 @@
 out=gpurun_out/sanitizer
 mkdir -p $out
 export SOM_SPIN_TIMEOUT_MS=900000
-CASES=${CASES:-"k1 k2 k3 k4 k5 k6 k9 map_exact map_sparse map_tc metrics batch"}
+CASES=${CASES:-"k1 k2 k3 k4 k5 k6 k10 map_exact map_sparse map_tc metrics batch"}
 TOOLS=${TOOLS:-"memcheck racecheck synccheck"}
 for tool in $TOOLS; do
   for c in $CASES; do

@@ -5,7 +5,7 @@ against the oracle (BMU log equal), so a run that "passes" the sanitizer
 with a wrong answer is visible.
 
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py k2
-  cases: k1 k2 k3 k4 k5 k6 k9 map_exact map_sparse map_tc metrics batch sharded2"""
+  cases: k1 k2 k3 k4 k5 k6 k10 k10b map_exact map_sparse map_tc metrics batch sharded2"""
 import os
 import sys
 import threading
@@ -77,8 +77,10 @@ elif case == "k5":
     train_case(16, 16, 64, 300, expect=5)
 elif case == "k6":
     train_case(10, 10, 512, 200, mode=som.SOM_TRAIN_W_REGISTERS, env={"SOM_TRAIN_SPEC": "1"}, expect=6)
-elif case == "k9":
-    train_case(20, 20, 4000, 400, csr=True, env={"SOM_TRAIN_ONCHIP": "1"}, expect=9, grid=16)
+elif case == "k10":
+    train_case(20, 20, 7600, 600, csr=True, expect=10, grid=20)
+elif case == "k10b":
+    train_case(20, 20, 6000, 600, csr=True, expect=10, grid=16)
 elif case == "map_exact":
     map_case(som.SOM_MAP_EXACT_F64, False)
 elif case == "map_sparse":
