@@ -13,10 +13,13 @@
 //                      (j < KJ) of a row as 4 KJ words of its TMEM lane
 //                      (lane quarter w % 4), column group (w - 1) / 4 (170
 //                      columns each), 4 KJ r; moved with tcgen05.ld/st (its
-//                      own path beside the shared-memory port);
+//                      own path beside the shared-memory port); updated rows
+//                      are also written through to W (the sparse sums below
+//                      gather from W, and only the owning warp can read a
+//                      TMEM lane);
 //   [ntm, non)         shared memory, [row][j][dt] float4 (conflict-free);
 //   [non, S)           W in global memory (L2-resident: only these rows are
-//                      touched during the launch), streamed through a ring of
+//                      read during the launch), streamed through a ring of
 //                      RC chunks (chunk j of a row = float4 [384 j, 384 j + 384)
 //                      = the thread's chunk j), filled by cp.async.bulk from
 //                      the control warp, full/empty mbarriers; updated rows
@@ -27,17 +30,17 @@
 //      alternating with on-chip rows so the ring keeps moving, branch-free:
 //      w' = fmaf(h, RN(x_{t-1} - w), w) (R11; x_{t-1} in registers, built
 //      once per step from its non-zeros) and |w'|^2 in fp64, per-warp
-//      partials by a multi-value butterfly over four rows; then S(x_t) of
-//      those rows: on-chip rows warp by warp over the union of the lanes'
-//      non-zeros of x_t (one TMEM word / shared-memory word per row and
-//      non-zero), streamed rows by one warp per row gathering from W;
-//      meanwhile the control warp feeds the ring;
+//      partials by a multi-value butterfly over two rows; then S(x_t) of
+//      those rows, one warp per row over x_t's non-zeros (shared-memory rows
+//      from shared memory, the others from W); meanwhile the control warp
+//      feeds the ring;
 //   2. barrier A; control warp: keys (updated units from the partials, the
 //      others from the speculative S of step 2' of the previous step), the
 //      exchange, the winner, h and the lists of update(t), first ring chunks
-//      of step t+1; data warps meanwhile (2'): bitmap of x_{t+1},
-//      speculative S(x_{t+1}) of every unit with its current row (exact for
-//      every unit update(t) leaves alone), list of x_{t+2};
+//      of step t+1 (one per lane); data warps meanwhile (2'): bitmap of
+//      x_{t+1}, speculative S(x_{t+1}) of every unit with its current row
+//      (exact for every unit update(t) leaves alone; skipped while the
+//      radius covers the lattice), list of x_{t+2};
 //   3. barrier B.
 // All sums have a fixed order (deterministic run to run).  At the end of the
 // launch the update of the last step is applied and the on-chip rows are
@@ -166,26 +169,34 @@ __device__ __noinline__ float list_lookup(const int* ci, const float* cv, int cn
     return (lo < cnt && ci[lo] == k) ? cv[lo] : 0.0f;
 }
 
+// position of column k in a sorted column list of cnt entries (-1 if absent)
+__device__ __noinline__ int list_pos(const int* ci, int cnt, int k) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return (lo < cnt && ci[lo] == k) ? lo : -1;
+}
+
 template <int KJ>
 __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs a, const TierPlan p) {
     __shared__ double pn[kSlots][NDW];        // |w'|^2 partials of dense-pass rows
-    __shared__ double ps[kSlots][NDW];        // S(x_t) partials of dense-pass on-chip rows
-    __shared__ double qs[2][kSlots][NDW];     // speculative S partials of on-chip rows, [parity of the step]
-    __shared__ double sg[2][kSlots];          // speculative S of streamed rows, [parity of the step]
-    __shared__ double sgd[kSlots];            // S(x_t) of dense-pass streamed rows
+    __shared__ double sg[2][kSlots];          // speculative S of every row, [parity of the step]
+    __shared__ double sgd[kSlots];            // S(x_t) of dense-pass rows
     __shared__ double wns[kSlots];            // fp64 |w_u|^2
     __shared__ float hs[kSlots];              // h of the pending update
     __shared__ int uid[kSlots];               // local unit (W row) of slot s
     __shared__ int ord[kSlots];               // dense-pass order of the pending update's rows
     __shared__ int strm[kSlots];              // its streamed rows, in ring order
+    __shared__ int iota[kSlots];              // 0, 1, 2, ... (every slot)
     __shared__ int s_nord, s_nstr, s_abort;
-    __shared__ unsigned s_onm;                // its on-chip rows (bit s)
     __shared__ long long nb[4][2];            // CSR bounds of x_t in nb[t & 3]
     __shared__ __align__(8) uint64_t full[kRingMax];
     __shared__ __align__(8) uint64_t empty[kRingMax];
     __shared__ uint32_t s_tmem;
     extern __shared__ __align__(128) float4 sm4[];
-    // sm4: ring [rc][NDT] | smem rows [nsm][KJ][NDT] | x cache float[2][4][NDT] | nzi int[3][cap] |
+    // sm4: ring [rc][NDT] | smem rows [nsm][KJ][NDT] | x cache float[2][2][NDT] | nzi int[3][cap] |
     //      nzv float[3][cap] | bitmap u32[2][bmw]
 
     const int b = blockIdx.x, G = a.G;
@@ -202,9 +213,9 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
     float4* W4 = reinterpret_cast<float4*>(a.W);
     float4* ring = sm4;
     float4* srows = sm4 + (size_t)RC * NDT;
-    // x_t at the thread's first 4 non-zeros: xcs[((t & 1) * 4 + rank) * NDT + dt]
+    // x_t at the thread's first 2 non-zeros: xcs[((t & 1) * 2 + rank) * NDT + dt]
     float* xcs = reinterpret_cast<float*>(srows + (size_t)nsm * KJ * NDT);
-    int* nzi = reinterpret_cast<int*>(xcs + 8 * NDT);
+    int* nzi = reinterpret_cast<int*>(xcs + 4 * NDT);
     float* nzv = reinterpret_cast<float*>(nzi + 3 * (size_t)cap);
     uint32_t* bmp = reinterpret_cast<uint32_t*>(nzv + 3 * (size_t)cap);
     // chunk KJ-1 is the only one that can run past the row (KJ = ceil(d4 / NDT))
@@ -257,21 +268,20 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         return m;
     };
     // x_t at this thread's element `bit` (set in mask m): the per-step cache
-    // holds the first 4 non-zeros in rank order; beyond, the sorted list
+    // holds the first 2 non-zeros in rank order; beyond, the sorted list
+    auto elem_k = [&](int bit) { return 4 * (dt + (bit >> 2) * NDT) + (bit & 3); };
     auto xget = [&](int64_t t, uint32_t m, int bit) {
         const int rank = __popc(m & ((1u << bit) - 1u));
-        if (rank < 4) return xcs[((int)(t & 1) * 4 + rank) * NDT + dt];
-        return list_lookup(nzi + (size_t)(t % 3) * cap, nzv + (size_t)(t % 3) * cap, cnt_of(t),
-                           4 * (dt + (bit >> 2) * NDT) + (bit & 3));
+        if (rank < 2) return xcs[((int)(t & 1) * 2 + rank) * NDT + dt];
+        return nzv[(size_t)(t % 3) * cap + list_pos(nzi + (size_t)(t % 3) * cap, cnt_of(t), elem_k(bit))];
     };
     auto fill_cache = [&](int64_t t, uint32_t m) {
         int rank = 0;
-        while (m != 0u && rank < 4) {
+        while (m != 0u && rank < 2) {
             const int bit = __ffs(m) - 1;
             m &= m - 1u;
-            xcs[((int)(t & 1) * 4 + rank) * NDT + dt] =
-                list_lookup(nzi + (size_t)(t % 3) * cap, nzv + (size_t)(t % 3) * cap, cnt_of(t),
-                            4 * (dt + (bit >> 2) * NDT) + (bit & 3));
+            const int q = list_pos(nzi + (size_t)(t % 3) * cap, cnt_of(t), elem_k(bit));
+            xcs[((int)(t & 1) * 2 + rank) * NDT + dt] = nzv[(size_t)(t % 3) * cap + q];
             ++rank;
         }
     };
@@ -307,77 +317,39 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         if (lane == 0) pn[pr0][dw] = tot;
         pr0 = -1;
     };
-    // S(x_tq) = sum over the thread's non-zeros of x_tq of (x - w)^2 - w^2 for
-    // the on-chip rows in `rows` (bit s), warp by warp over the union of the
-    // lanes' non-zeros; per-warp partials -> dst[s][dw].  q[0..7] = TMEM
-    // slots 0..7, q[8..11] = shared-memory slots ntm..ntm+3 (static indices).
-    auto onchip_sparse = [&](int64_t tq, uint32_t mq, uint32_t rows, double (*dst)[NDW]) {
-        double q[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) q[i] = 0.0;
-        for (uint32_t M = __reduce_or_sync(0xffffffffu, mq); M != 0u; M &= M - 1u) {
-            const int bit = __ffs(M) - 1;
-            const bool mine = (mq >> bit) & 1u;
-            const float x = mine ? xget(tq, mq, bit) : 0.0f;
-            const int j = bit >> 2, c = bit & 3;
-            uint32_t v[kTmMax];
-#pragma unroll
-            for (int s = 0; s < kTmMax; ++s)
-                if (s < ntm && ((rows >> s) & 1u))
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v[s]) : "r"(tm_addr(s) + (uint32_t)bit));
-            twait_ld();
-            if (mine) {
-#pragma unroll
-                for (int s = 0; s < kTmMax; ++s)
-                    if (s < ntm && ((rows >> s) & 1u)) q[s] += sterm(x, __uint_as_float(v[s]));
-#pragma unroll
-                for (int s2 = 0; s2 < kSmMax; ++s2) {
-                    if (s2 >= nsm || !((rows >> (ntm + s2)) & 1u)) continue;
-                    const float w = reinterpret_cast<const float*>(srows + ((size_t)s2 * KJ + j) * NDT + dt)[c];
-                    q[8 + s2] += sterm(x, w);
-                }
+    // S(x_t) = sum_p (x_p - w_p)^2 - w_p^2 over x_t's non-zeros p, one warp
+    // per row, two rows per warp at a time (multi-value butterfly); each row
+    // with its current value: shared-memory rows from shared memory, the
+    // others from W in global memory (streamed rows are current, TMEM rows
+    // are written through)
+    auto fetch = [&](int s, int k) {
+        if (s >= ntm && s < non) {
+            const int e = k >> 2, j = e / NDT, d = e - j * NDT;
+            return reinterpret_cast<const float*>(srows + ((size_t)(s - ntm) * KJ + j) * NDT + d)[k & 3];
+        }
+        return __ldcg(a.W + (int64_t)uid[s] * a.dimp + k);
+    };
+    auto sparse_rows = [&](int64_t tq, const int* slots, int count, double* dst) {
+        const int cnt = cnt_of(tq);
+        const int* ci = nzi + (size_t)(tq % 3) * cap;
+        const float* cv = nzv + (size_t)(tq % 3) * cap;
+        for (int i = dw; i < count; i += 2 * NDW) {
+            const bool two = i + NDW < count;
+            const int sa = slots[i], sb2 = two ? slots[i + NDW] : sa;
+            double va = 0.0, vb = 0.0;
+            for (int q = lane; q < cnt; q += 32) {
+                const float x = cv[q];
+                const int k = ci[q];
+                const float wa = fetch(sa, k);
+                const float wb = two ? fetch(sb2, k) : 0.f;
+                va += sterm(x, wa);
+                vb += sterm(x, wb);
             }
+            double v2[2] = {va, vb};
+            int sl = 0;
+            const double tot = butterfly_sum<2>(v2, lane, &sl);
+            if ((lane & 15) == 0 && (sl == 0 || two)) dst[sl ? sb2 : sa] = tot;
         }
-        int sl = 0;
-        const double tot = butterfly_sum<16>(q, lane, &sl);
-        const int s = sl < 8 ? sl : ntm + (sl - 8);
-        if ((lane & 1) == 0 && (sl < 8 ? sl < ntm : sl - 8 < nsm) && s < non && ((rows >> s) & 1u)) dst[s][dw] = tot;
-    };
-    // S(x_tq) of streamed rows (list of slots), one warp per row gathering
-    // over the non-zeros of x_tq from W (global, L2)
-    auto stream_sparse = [&](int64_t tq, const int* slots, int count, double* dst) {
-        const int cnt = cnt_of(tq);
-        const int* ci = nzi + (size_t)(tq % 3) * cap;
-        const float* cv = nzv + (size_t)(tq % 3) * cap;
-        for (int i = dw; i < count; i += NDW) {
-            const int s = slots ? slots[i] : non + i;
-            const float* row = a.W + (int64_t)uid[s] * a.dimp;
-            double v = 0.0;
-            for (int q = lane; q < cnt; q += 32) v += sterm(cv[q], __ldcg(row + ci[q]));
-            v = warp_sum_f64(v);
-            if (lane == 0) dst[s] = v;
-        }
-    };
-    // the dense pass's streamed rows (at most one per warp when count <= 12):
-    // the gather's loads are issued before the on-chip sums and finished after
-    auto stream_issue = [&](int64_t tq, int count, float (&g)[2]) {
-        g[0] = g[1] = 0.0f;
-        if (dw >= count) return;
-        const int cnt = cnt_of(tq);
-        const int* ci = nzi + (size_t)(tq % 3) * cap;
-        const float* row = a.W + (int64_t)uid[strm[dw]] * a.dimp;
-        if (lane < cnt) g[0] = __ldcg(row + ci[lane]);
-        if (lane + 32 < cnt) g[1] = __ldcg(row + ci[lane + 32]);
-    };
-    auto stream_finish = [&](int64_t tq, int count, const float (&g)[2]) {
-        if (dw >= count) return;
-        const int cnt = cnt_of(tq);
-        const float* cv = nzv + (size_t)(tq % 3) * cap;
-        double v = 0.0;
-        if (lane < cnt) v += sterm(cv[lane], g[0]);
-        if (lane + 32 < cnt) v += sterm(cv[lane + 32], g[1]);
-        v = warp_sum_f64(v);
-        if (lane == 0) sgd[strm[dw]] = v;
     };
 
     // ---- prologue
@@ -387,7 +359,6 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         if (lane == 0) {
             s_abort = 0;
-            s_onm = 0u;
             s_nord = 0;
             s_nstr = 0;
             for (int r = 0; r < RC; ++r) {
@@ -401,7 +372,7 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         }
     }
     for (int s = tid; s < Sb; s += NTH) uid[s] = a.utab ? a.utab[(size_t)b * a.S + s] : b + s * G;
-    for (int s = tid; s < kSlots; s += NTH) hs[s] = 0.0f;
+    for (int s = tid; s < kSlots; s += NTH) { hs[s] = 0.0f; iota[s] = s; }
     tc_before();
     __syncthreads();
     tc_after();
@@ -435,9 +406,8 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         build_bitmap(a.t0);
         mc = mask_of(a.t0);
         fill_cache(a.t0, mc);
-        // speculative S(x_t0) of every unit (no update is pending)
-        onchip_sparse(a.t0, mc, 0xffffffffu, qs[a.t0 & 1]);
-        stream_sparse(a.t0, nullptr, Sb - non, sg[a.t0 & 1]);
+        // speculative S(x_t0) of every unit (no update is pending; W is current)
+        sparse_rows(a.t0, iota, Sb, sg[a.t0 & 1]);
     }
     tc_before();
     __syncthreads();
@@ -465,9 +435,9 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
     double f_next = a.t1 > a.t0 ? a.f_tab[0] : 0.0;   // decay factor of the coming step, loaded a step ahead
     for (int64_t t = a.t0; t < a.t1; ++t) {
         // phase trace (som_set_trace): control lane 0 stamps [0] loop top,
-        // [3] keys formed, [4] winner known, [5] lists + ring issued, [6]
-        // after barrier B; data thread 0 stamps [1] dense pass done, [2]
-        // sparse sums done
+        // [3] keys formed, [4] winner known; data thread 0 stamps [1] dense
+        // pass done, [2] its sparse sums done, [5] bitmap + x cache of
+        // x_{t+1} done, [6] speculative on-chip sums done, [7] phase 2' done
         unsigned long long* tr = nullptr;
         unsigned long long* tr1 = nullptr;
         if (a.trace && t - a.t0 < a.trace_steps) {
@@ -477,21 +447,32 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
         }
         if (tr) tr[0] = trace_now(a.trace_clk);
         const double f = f_next;
+        const double alpha = a.alpha0 * f;
+        double sigma = a.sigma0 * f;
+        if (sigma < a.sigma_min) sigma = a.sigma_min;
+        const double two_s2 = 2.0 * sigma * sigma;
+        const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
+        // speculative sums run in 2' of this step unless the radius covers
+        // the lattice (every unit then takes the next dense pass)
+        const bool spec = !(r2 >= a.g2max);
         // ---- 1. dense pass over update(t-1)'s rows: Eq. 1 with x_{t-1}
-        // (registers), |w'|^2; then S(x_t) of those rows
+        // (registers), |w'|^2 (TMEM rows written through to W); then S(x_t)
+        // of those rows
         if (data) {
-            const int nord = s_nord, nstr = s_nstr;
+            const int nord = s_nord;
             if (nord > 0) build_xp(t - 1, mp);
             for (int i = 0; i < nord; ++i) {
                 const int s = ord[i];
                 const float h = hs[s];
                 double n0 = 0.0, n1 = 0.0;
+                float4* grow = W4 + (int64_t)uid[s] * d4 + dt;
                 if (s < ntm) {
                     float4 w[KJ];
                     tm_load<KJ>(tm_addr(s), w);
 #pragma unroll
                     for (int j = 0; j < KJ; ++j) {
                         w[j] = eq1u(h, w[j], xp[j]);
+                        if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, w[j]);   // write-through
                         const double e0 = w[j].x, e1 = w[j].y, e2 = w[j].z, e3 = w[j].w;
                         n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
                     }
@@ -506,7 +487,6 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
                         n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
                     }
                 } else {
-                    float4* grow = W4 + (int64_t)uid[s] * d4 + dt;
 #pragma unroll
                     for (int j = 0; j < KJ; ++j) {
                         mbar_wait_g(&full[cslot], (uint32_t)(cu & 1));
@@ -526,37 +506,29 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
             push_flush();
             twait_st();
             if (tr1) tr1[1] = trace_now(a.trace_clk);
-            const bool short_list = nstr <= NDW && cnt_of(t) <= 64;
-            float g[2];
-            if (nstr > 0) {
-                // streamed rows written above: visible to the gathers below
-                // (generic) and to the next ring fill (async proxy)
+            if (nord > 0) {
+                // rows written above: visible to the gathers below (generic)
+                // and to the next ring fill (async proxy)
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 bar_data();
-                if (short_list) stream_issue(t, nstr, g);
-            }
-            if (s_onm != 0u) onchip_sparse(t, mc, s_onm, ps);
-            if (nstr > 0) {
-                if (short_list) stream_finish(t, nstr, g);
-                else stream_sparse(t, strm, nstr, sgd);
+                sparse_rows(t, ord, nord, sgd);
             }
             if (tr1) tr1[2] = trace_now(a.trace_clk);
-        } else if (lane == 0) {
-            // ring producer: the rest of this step's streamed chunks
-            const int total = s_nstr * KJ;
-            for (int c = issued; c < total; ++c) produce(c);
+        } else {
+            // ring producer (lane 0): the rest of this step's streamed chunks
+            if (lane == 0) {
+                const int total = s_nstr * KJ;
+                for (int c = issued; c < total; ++c) produce(c);
+            }
             issued = 0;
+            pslot = __shfl_sync(0xffffffffu, pslot, 0);
+            pu = __shfl_sync(0xffffffffu, pu, 0);
         }
         tc_before();
         __syncthreads();   // (A) pass done: partials complete, rows stored
         tc_after();
 
         if (t + 1 < a.t1) f_next = a.f_tab[t + 1 - a.t0];
-        const double alpha = a.alpha0 * f;
-        double sigma = a.sigma0 * f;
-        if (sigma < a.sigma_min) sigma = a.sigma_min;
-        const double two_s2 = 2.0 * sigma * sigma;
-        const double r2 = a.cutoff_on ? two_s2 * a.ln_inv_eps : INFINITY;
 
         if (!data) {
             // ---- 2. control warp: keys, exchange, winner, lists of update(t)
@@ -564,22 +536,11 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
             if (lane < Sb) {
                 double tot;
                 if (my_upd) {
-                    double nn = 0.0, sv = 0.0;
+                    double nn = 0.0;
 #pragma unroll
                     for (int w8 = 0; w8 < NDW; ++w8) nn += pn[lane][w8];
-                    if (lane < non) {
-#pragma unroll
-                        for (int w8 = 0; w8 < NDW; ++w8) sv += ps[lane][w8];
-                    } else {
-                        sv = sgd[lane];
-                    }
                     wns[lane] = nn;
-                    tot = nn + sv;
-                } else if (lane < non) {
-                    double sv = 0.0;
-#pragma unroll
-                    for (int w8 = 0; w8 < NDW; ++w8) sv += qs[t & 1][lane][w8];
-                    tot = wns[lane] + sv;
+                    tot = nn + sgd[lane];
                 } else {
                     tot = wns[lane] + sg[t & 1][lane];
                 }
@@ -621,17 +582,25 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
             }
             __syncwarp();
             if (lane == 0) {
-                s_onm = onm;
                 s_nord = ns + no;
                 s_nstr = ns;
-                // first chunks of the next pass into the ring (none after the
-                // last step: the flush reads streamed rows directly)
-                if (!stop && t + 1 < a.t1) {
-                    const int first = min(RC, ns * KJ);
-                    for (int cch = 0; cch < first; ++cch) produce(cch);
-                    issued = first;
+            }
+            // first chunks of the next pass into the ring, one per lane (none
+            // after the last step: the flush reads streamed rows directly)
+            if (!stop && t + 1 < a.t1) {
+                const int first = min(RC, ns * KJ);
+                if (lane < first) {
+                    int slot = pslot + lane, u = pu;
+                    if (slot >= RC) { slot -= RC; ++u; }
+                    const int row = strm[lane / KJ], j = lane % KJ;
+                    if (u > 0) mbar_wait_g(&empty[slot], (uint32_t)((u - 1) & 1));
+                    const int nf4 = min(NDT, d4 - j * NDT);
+                    bulk_row(ring + (size_t)slot * NDT, W4 + (int64_t)uid[row] * d4 + (size_t)j * NDT,
+                             (uint32_t)nf4 * 16u, &full[slot]);
                 }
-                if (tr) tr[5] = trace_now(a.trace_clk);
+                pslot += first;
+                if (pslot >= RC) { pslot -= RC; ++pu; }
+                issued = first;
             }
         } else {
             // ---- 2'. data warps: list of x_{t+2}, bounds of x_{t+3}, bitmap
@@ -645,24 +614,23 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
                 build_bitmap(t + 1);
                 mn = mask_of(t + 1);
                 fill_cache(t + 1, mn);
-                if (!(r2 >= a.g2max)) {
-                    onchip_sparse(t + 1, mn, 0xffffffffu, qs[(t + 1) & 1]);
-                    stream_sparse(t + 1, nullptr, Sb - non, sg[(t + 1) & 1]);
-                }
+                if (tr1) tr1[5] = trace_now(a.trace_clk);
+                if (spec) sparse_rows(t + 1, iota, Sb, sg[(t + 1) & 1]);
+                if (tr1) tr1[6] = trace_now(a.trace_clk);
             }
             cp_async_wait_all();
             mp = mc;
             mc = mn;
+            if (tr1) tr1[7] = trace_now(a.trace_clk);
         }
         tc_before();
         __syncthreads();   // (B)
         tc_after();
-        if (tr) tr[6] = trace_now(a.trace_clk);
         if (s_abort) break;
     }
 
-    // flush the update of the last step (sample x_{t1-1}), then write every
-    // on-chip row back to W
+    // flush the update of the last step (sample x_{t1-1}) into the rows'
+    // storage, then write every on-chip row back to W
     if (data && a.t1 > a.t0 && !s_abort) {
         const int nord = s_nord;
         if (nord > 0) build_xp(a.t1 - 1, mp);
@@ -687,8 +655,6 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
             }
         }
         twait_st();
-    }
-    if (data && !s_abort) {
         for (int s = 0; s < non; ++s) {
             float4 w[KJ];
             if (s < ntm) {
@@ -709,16 +675,17 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512) : "memory");
 }
 
-constexpr size_t kTierStatic = (2 * kSlots * NDW + 2 * kSlots * NDW) * 8 + (2 * kSlots + 2 * kSlots) * 8 + 1024 + 512;
+constexpr size_t kTierStatic = kSlots * NDW * 8 + 4 * kSlots * 8 + 5 * kSlots * 4 + 1024 + 512;
 
-size_t tier_smem_bytes(int kj, int dimp, int cap, const TierPlan& p) {
-    return sizeof(float4) * (size_t)NDT * ((size_t)p.rc + (size_t)p.nsm * kj) + 8 * 4 * (size_t)NDT + 24 * (size_t)cap +
+size_t tier_smem_bytes(int /*S*/, int kj, int dimp, int cap, const TierPlan& p) {
+    return sizeof(float4) * (size_t)NDT * ((size_t)p.rc + (size_t)p.nsm * kj) + 4 * 4 * (size_t)NDT +
+           24 * (size_t)cap +
            8 * (size_t)((dimp >> 5) + 1) + 128;
 }
 
 template <int KJ>
 cudaError_t launch_tier_kj(const TrainArgs& a, const TierPlan& p, cudaStream_t st) {
-    const size_t smem = tier_smem_bytes(KJ, a.dimp, a.nz_cap, p);
+    const size_t smem = tier_smem_bytes(a.S, KJ, a.dimp, a.nz_cap, p);
     auto fn = som_train_tier_kernel<KJ>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -746,13 +713,13 @@ bool tier_plan(int S, int dimp, int maxnnz, int max_smem_optin, TierPlan* out) {
     const int rest = S - p.ntm;
     p.nsm = std::max(0, std::min(smax, rest));
     p.rc = rest > p.nsm ? rc_min : 2;
-    while (p.nsm > 0 && tier_smem_bytes(kj, dimp, cap, p) > budget) --p.nsm;
+    while (p.nsm > 0 && tier_smem_bytes(S, kj, dimp, cap, p) > budget) --p.nsm;
     if (S - p.ntm - p.nsm > 0) p.rc = rc_min;
-    if (tier_smem_bytes(kj, dimp, cap, p) > budget) return false;
+    if (tier_smem_bytes(S, kj, dimp, cap, p) > budget) return false;
     while (p.rc < rc_max && S - p.ntm - p.nsm > 0) {
         TierPlan q = p;
         ++q.rc;
-        if (tier_smem_bytes(kj, dimp, cap, q) > budget) break;
+        if (tier_smem_bytes(S, kj, dimp, cap, q) > budget) break;
         p = q;
     }
     *out = p;

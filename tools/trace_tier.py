@@ -31,13 +31,17 @@ t = tr.view(148, steps, 8)[:G].cpu().numpy().astype(np.float64)[:, 50:]
 print(f"t=[{tb},{tb + steps}) G={G} kernel={k}: {1000 * ms / units:.3f} us/step (event)")
 if k == 10:
     seg = [("top -> dense pass done", 0, 1), ("dense -> sparse sums done", 1, 2), ("sparse -> keys (barrier A)", 2, 3),
-           ("keys -> winner (exchange)", 3, 4), ("winner -> lists+ring", 4, 5), ("lists -> after barrier B", 5, 6)]
+           ("keys -> winner (exchange)", 3, 4), ("A -> bitmap+cache (2')", 3, 5), ("cache -> onchip spec", 5, 6),
+           ("onchip spec -> 2' done", 6, 7)]
 else:
     seg = [(f"[{i}] -> [{i + 1}]", i, i + 1) for i in range(6)]
 for name, i, j in seg:
     dd = t[:, :, j] - t[:, :, i]
     med = np.median(dd, axis=1)
-    print(f"  {name:28s} median over CTAs {np.median(med):7.0f} ns  min {med.min():7.0f}  max {med.max():7.0f}")
+    print(f"  {name:28s} median over CTAs {np.median(med):7.0f} ns  min {med.min():7.0f}  max {med.max():7.0f}"
+          f"   per-step max over CTAs: median {np.median(dd.max(0)):7.0f}  p90 {np.percentile(dd.max(0), 90):7.0f}")
+top = t[:, :, 0]
+print(f"  loop-top spread per step: median {np.median(top.max(0) - top.min(0)):.0f} ns")
 loop = np.diff(t[:, :, 0], axis=1)
 print(f"  loop period median {np.median(loop):.0f} ns")
 pub = t[:, :, 3]
