@@ -188,10 +188,12 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * range, 2 = kernel 7 (needs >= 8192 prototype elements per CTA and no
  * forced mode or grid).  Kernel 8 = the NCCL step path (som_set_exchange).
  * Kernel 10 = CSR input (or sparse dense rows, converted on the device) in
- * AUTO mode where W does not fit the SMs' shared memory, with the
- * environment variable SOM_TRAIN_TIER=1: the map held in tensor memory and
- * shared memory, the rest streamed through a TMA ring (train_tier.cu);
- * kernel 4 otherwise.
+ * AUTO mode where W does not fit the SMs' shared memory: the map held in
+ * tensor memory and shared memory, the rest streamed through a TMA ring
+ * (train_tier.cu).  It runs while the neighbourhood covers the whole
+ * lattice and kernel 4 after (kernel 11 = both, two launches in one call;
+ * SOM_TIER_HANDOVER=0 keeps kernel 10, SOM_TRAIN_TIER=0 selects kernel 4
+ * throughout).
  * All follow the same arithmetic contract (R9-R11). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 

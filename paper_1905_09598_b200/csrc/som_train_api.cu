@@ -218,9 +218,8 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     bool dense_csr = true;
     if (const char* e = std::getenv("SOM_TRAIN_DENSE_CSR")) dense_csr = std::atoi(e) != 0;
     // kernel 10 (train_tier.cu) for CSR rows where W streams from global
-    // memory in AUTO mode: opt-in (SOM_TRAIN_TIER=1) while it is slower than
-    // kernel 4 on c3 (kernel 10)
-    bool tier_env = false;
+    // memory in AUTO mode (SOM_TRAIN_TIER=0: kernel 4 throughout)
+    bool tier_env = true;
     if (const char* e = std::getenv("SOM_TRAIN_TIER")) tier_env = std::atoi(e) != 0;
     tier_env = tier_env && h->train_mode == SOM_TRAIN_AUTO && !use_small && !use_reg && !a.w_smem;
     if (!csr && dense_csr && !use_small && !use_reg && !a.w_smem && a.x_vec4 &&
@@ -314,6 +313,30 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     const char* spec_env = std::getenv("SOM_TRAIN_SPEC");
     const int spec_mode = spec_env ? std::atoi(spec_env) : 0;
     if (use_reg && spec_mode == 1 && train_spec_supported(a.S, h->dim, a.G, h->world)) use_spec = true;
+    // kernel 10 while the neighbourhood covers the whole lattice (every unit
+    // updated every step: its on-chip rows save the most), then kernel 4
+    // (few updated units: kernel 4's step is shorter); an exact t-range
+    // split, both kernels give identical results.  SOM_TIER_HANDOVER=0:
+    // kernel 10 throughout.
+    int64_t t_tier = t_end;
+    if (use_tier && a.cutoff_on) {
+        bool handover = true;
+        if (const char* e = std::getenv("SOM_TIER_HANDOVER")) handover = std::atoi(e) != 0;
+        if (handover) {
+            auto full_cover = [&](int64_t t) {
+                double f;
+                fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
+                const double sigma = std::max(sd.sigma_min, sigma0 * f);
+                return 2.0 * sigma * sigma * a.ln_inv_eps >= a.g2max;
+            };
+            int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) not fully covered
+            while (lo < hi) {
+                const int64_t mid = lo + (hi - lo) / 2;
+                if (full_cover(mid)) lo = mid + 1; else hi = mid;
+            }
+            t_tier = lo;
+        }
+    }
     int64_t t_split = t_begin;   // hybrid: kernel 6 on [t_begin, t_split), kernel 2 after
     int G6 = 0;
     if (use_reg && spec_mode == 2 && h->train_mode == SOM_TRAIN_AUTO && h->train_grid == 0 && h->world == 1 &&
@@ -419,7 +442,25 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         }
     }
     else if (use_reg) CK(launch_train_reg(a, h->stream));
-    else if (use_tier) CK(launch_train_tier(a, h->max_smem_optin, h->stream));
+    else if (use_tier) {
+        if (t_tier > t_begin) {
+            TrainArgs a10 = a;
+            a10.t1 = t_tier;
+            CK(launch_train_tier(a10, h->max_smem_optin, h->stream));
+        }
+        if (t_tier < t_end) {
+            // kernel 4 from the first step whose radius no longer covers the
+            // lattice (fresh exchange slots; the abort flag stays)
+            if (t_tier > t_begin) CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords, h->stream));
+            TrainArgs a4 = a;
+            a4.t0 = t_tier;
+            a4.f_tab = a.f_tab + (t_tier - t_begin);
+            if (a4.bmu_log) a4.bmu_log = a.bmu_log + (t_tier - t_begin);
+            if (t_tier > t_begin) { a4.trace = nullptr; a4.trace_steps = 0; }
+            CK(launch_train_csr(a4, h->stream));
+            if (t_tier > t_begin) launches = 2;
+        }
+    }
     else if (use_csr) CK(launch_train_csr(a, h->stream));
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
@@ -429,7 +470,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_tier ? 10 : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_tier ? (t_tier >= t_end ? 10 : t_tier > t_begin ? 11 : 4) : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

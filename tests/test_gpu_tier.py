@@ -21,7 +21,8 @@ KERNEL_TIER = 10
 
 @pytest.fixture(autouse=True)
 def _tier_on(monkeypatch):
-    monkeypatch.setenv("SOM_TRAIN_TIER", "1")   # kernel 10 is opt-in
+    monkeypatch.setenv("SOM_TRAIN_TIER", "1")
+    monkeypatch.setenv("SOM_TIER_HANDOVER", "0")   # kernel 10 for the whole range
 
 
 @pytest.fixture(scope="module")
@@ -150,3 +151,17 @@ def test_tier_c3_late_window_equals_kernel4(som, monkeypatch):
     assert out["0"][0] == 4 and out["1"][0] == KERNEL_TIER
     assert np.array_equal(out["0"][2], out["1"][2])
     assert np.array_equal(out["0"][1], out["1"][1])
+
+
+def test_tier_handover_to_kernel4(som, monkeypatch):
+    """AUTO with SOM_TRAIN_TIER=1: kernel 10 while the neighbourhood covers
+    the lattice, kernel 4 from the first step where it does not (kernel id
+    11, two launches): the whole schedule against the oracle."""
+    monkeypatch.setenv("SOM_TIER_HANDOVER", "1")
+    C = bank_corpus(300, 8000, seed=91)
+    X = C.dense()
+    W0 = init_rows(X, 40 * 40, 91)
+    W, log, k = _run(som, 40, 40, C, W0, 3, 20.0, 9, grid=64)
+    assert k == 11, k
+    Wo, logo = oracle.train_online(W0, 40, 40, 1, X, 3, 0.1, 20.0, 9)
+    _check(W, log, Wo, logo)
