@@ -675,9 +675,10 @@ def run_b200(args, rank, world, local):
         som.som_set_stream(md.h, stream)
         sdist.init_nccl(md.h, rank, world, som.SOM_SHARD_DOCS)
         lo, hi = sdist.shard_range(n, rank, world)
-        srp = (rp[lo:hi + 1] - rp[lo]).contiguous()
-        sci, sva = ci[int(C.indptr[lo]):int(C.indptr[hi])], va[int(C.indptr[lo]):int(C.indptr[hi])]
         ns = hi - lo
+        h_srp = (C.indptr[lo:hi + 1] - C.indptr[lo]).astype(np.int64)
+        h_sci, h_sva = C.indices[C.indptr[lo]:C.indptr[hi]], C.data[C.indptr[lo]:C.indptr[hi]]
+        srp, sci, sva = (torch.from_numpy(np.ascontiguousarray(x)).cuda(local) for x in (h_srp, h_sci, h_sva))
         b1 = torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")
         b2 = torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")
         d1 = torch.empty(max(ns, 1), dtype=torch.float32, device="cuda")
@@ -686,29 +687,41 @@ def run_b200(args, rank, world, local):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
 
         def one_step(ins, outs):
+            # ins: the full CSR corpus (every rank trains on all of it) and this
+            # rank's document shard; outs: its bmu1, bmu2, D1 and the U-matrix
+            # (device tensors, or pinned host buffers for e2e)
+            irp, ici, iva, jrp, jci, jva = ins
+            ob1, ob2, od1, oU = outs
+            launches = 0
             evs[0].record(stream)
-            som.som_init_random_csr(sm.h, rp, ci, va, n, init_seed)
+            som.som_init_random_csr(sm.h, irp, ici, iva, n, init_seed)
+            launches += som.som_last_stats(sm.h)[2]
             evs[1].record(stream)
             dist.barrier()
-            som.som_train_online_csr(sm.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, -1, None)
-            train_ms = som.som_last_stats(sm.h)[0]
+            som.som_train_online_csr(sm.h, irp, ici, iva, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, -1,
+                                     None)
+            train_ms, _, tl = som.som_last_stats(sm.h)
+            launches += tl
             dist.barrier()
             evs[2].record(stream)
             Wfull.zero_()
             som.som_get_weights(sm.h, Wfull)                 # own rows; all-reduce assembles the map
             dist.all_reduce(Wfull)
             md.set_weights(Wfull)
-            som.som_map_csr(md.h, srp, sci, sva, ns, b1, b2, d1)
+            som.som_map_csr(md.h, jrp, jci, jva, ns, ob1, ob2, od1)
+            launches += som.som_last_stats(md.h)[2]
             evs[3].record(stream)
-            qe, te = som.som_errors_csr(md.h, srp, sci, sva, ns)   # NCCL-reduced inside libsom
+            qe, te = som.som_errors_csr(md.h, jrp, jci, jva, ns)   # NCCL-reduced inside libsom
+            launches += som.som_last_stats(md.h)[2]
             evs[4].record(stream)
-            som.som_umatrix(md.h, U)
+            som.som_umatrix(md.h, oU)
+            launches += som.som_last_stats(md.h)[2]
             evs[5].record(stream)
             torch.cuda.synchronize()
             ph = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
             return {"phase_ms": dict(zip(["init", "train", "map (gather W + shard)", "errors", "umatrix"], ph)),
-                    "train_kernel_ms": train_ms, "launches": 0, "qe": qe, "te": te}
-        dev_in, dev_out = None, None
+                    "train_kernel_ms": train_ms, "launches": launches, "qe": qe, "te": te}
+        dev_in, dev_out = (rp, ci, va, srp, sci, sva), (b1, b2, d1, U)
 
     for _ in range(max(3, args.warmup)):
         one_step(dev_in, dev_out)
@@ -736,26 +749,36 @@ def run_b200(args, rank, world, local):
     total_ms = float(t_max.item())
     value = args.steps * T / (total_ms / 1e3)
 
-    # ---- e2e: the same call with pinned HOST inputs and host outputs
-    e2e = None
+    # ---- e2e: the same calls with pinned HOST inputs and host outputs
+    hfull = tuple(torch.from_numpy(a).pin_memory() for a in (C.indptr, C.indices, C.data))
     if world == 1:
-        hin = tuple(torch.from_numpy(a).pin_memory() for a in (C.indptr, C.indices, C.data))
-        hout = (torch.empty(n, dtype=torch.int32).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
-                torch.empty(n, dtype=torch.float32).pin_memory(), torch.empty(N, dtype=torch.float32).pin_memory())
-        e2e_ms = []
-        for _ in range(max(1, min(args.steps, 3))):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            one_step(hin, hout)
-            torch.cuda.synchronize()
-            e2e_ms.append(1e3 * (time.perf_counter() - t0))
-        h2d = int(C.indptr.nbytes + C.indices.nbytes + C.data.nbytes)
-        d2h = 12 * n + 4 * N + 16
-        e2e = {"value": T / (statistics.mean(e2e_ms) / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
-               "what": "som_fit_csr with pinned host CSR arrays (staged once per call) and host outputs (bmu1, bmu2, "
-                       "D1, U, QE, TE), wall clock per call"}
+        hin, nd = hfull, n
+    else:
+        hin = hfull + tuple(torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (h_srp, h_sci, h_sva))
+        nd = ns
+    hout = (torch.empty(max(nd, 1), dtype=torch.int32).pin_memory(),
+            torch.empty(max(nd, 1), dtype=torch.int32).pin_memory(),
+            torch.empty(max(nd, 1), dtype=torch.float32).pin_memory(), torch.empty(N, dtype=torch.float32).pin_memory())
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        one_step(hin, hout)
+        torch.cuda.synchronize()
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_mean = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_mean, op=dist.ReduceOp.MAX)
+    h2d = sum(int(x.numel() * x.element_size()) for x in hin)
+    d2h = sum(int(x.numel() * x.element_size()) for x in hout) + 16
+    e2e = {"value": T / (float(e2e_mean.item()) / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h,
+           "what": ("som_fit_csr" if world == 1 else "the sharded step's libsom calls") +
+                   " with pinned host CSR arrays (staged once per call) and host outputs (bmu1, bmu2, D1, U, QE, "
+                   "TE), wall clock per step" + ("" if world == 1 else ", max over ranks; bytes of rank 0")}
 
     # ---- roofline of the dominant kernel (the training kernel of the step)
     train_ms = statistics.mean(i["train_kernel_ms"] for i in infos)
@@ -769,7 +792,7 @@ def run_b200(args, rank, world, local):
         som.som_train_online_csr(m.h, rp, ci, va, n, cfg["epochs"], ALPHA0, cfg["sigma0"], None, seed, 0, -1, log)
         H = updated_units(cfg["rows"], cfg["cols"], cfg["topo"], log.cpu().numpy(), 0, T, cfg["sigma0"])
         nnz_x = C.nnz / n
-        sparse = k_used in (4, 9)
+        sparse = k_used in (4, 10, 11)
         algo = train_bytes(N, d, nnz_x, H, sparse)
         gbps = algo / (train_ms / 1e3) / 1e9
         l2, l2src = l2_peak_gbs(96)
@@ -781,7 +804,10 @@ def run_b200(args, rank, world, local):
                 tj = json.load(f)
             traffic = tj.get("bytes_per_launch")
         kname = {3: "som_train_tma_kernel (dense rows, W streamed)", 4: "som_train_csr_tma_kernel (sparse distances, "
-                 "W streamed through L2)", 2: "som_train_reg_kernel (W in registers)"}.get(k_used, f"kernel {k_used}")
+                 "W streamed through L2)", 2: "som_train_reg_kernel (W in registers)",
+                 10: "som_train_tier_kernel (W in TMEM + smem + a streamed remainder, sparse distances)",
+                 11: "som_train_tier_kernel while the neighbourhood covers the map, then som_train_csr_tma_kernel "
+                     "(sparse distances)"}.get(k_used, f"kernel {k_used}")
         roof = {"bound": "l2", "kernel": f"{kname}, G={g_used}", "achieved": gbps, "peak": l2, "unit": "GB/s",
                 "frac": gbps / l2, "traffic": traffic, "peak_source": l2src, "hbm_frac": gbps / hbm,
                 "hbm_peak_source": hsrc,
@@ -836,7 +862,7 @@ def run_b200(args, rank, world, local):
                       "us_per_training_step": 1e3 * train_ms / T, "phase_ms": ph_mean,
                       "qe": infos[-1]["qe"], "te": infos[-1]["te"], "train_kernel": k_used, "grid": g_used},
         "e2e": e2e,
-        "gpu_launches": infos[-1]["launches"] * args.steps if world == 1 else None,
+        "gpu_launches": infos[-1]["launches"] * args.steps,
         "roofline": roof,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
