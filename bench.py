@@ -228,6 +228,23 @@ def train_bytes(N, d, nnz_x, H, sparse):
     return float(np.sum(4.0 * N * d + 4.0 * H * d + 4.0 * d))
 
 
+def nccl_usable():
+    """NCCL refuses two ranks on one GPU: the one-device plumbing hook
+    (BENCH_ONE_DEVICE=1) reduces the document-sharded error sums over
+    torch.distributed instead and skips the NCCL exchange baseline."""
+    return os.environ.get("BENCH_ONE_DEVICE") != "1"
+
+
+def sharded_errors(som, h, rp, ci, va, n, world):
+    """QE/TE of a document-sharded corpus: inside libsom over its NCCL
+    communicator, or (one-device hook) this rank's values reduced here."""
+    if world == 1 or nccl_usable():
+        return som.som_errors_csr(h, rp, ci, va, n)
+    from paper_1905_09598_b200 import dist as sdist
+    qe, te = som.som_errors_csr(h, rp, ci, va, n) if n > 0 else (0.0, 0.0)
+    return sdist.reduce_errors(qe, te, n, device="cuda")
+
+
 def config_dict(name, cfg, world):
     """The config both arms report (identical keys and values)."""
     return {"workload": name, "map": f"{cfg['rows']}x{cfg['cols']} {'hex' if cfg['topo'] else 'rect'}",
@@ -294,7 +311,7 @@ def c5_leg(som, torch, args, local, rank, world, corpus):
     W = torch.from_numpy(c5_codebook()).cuda(local)
     mm = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
     som.som_set_stream(mm.h, torch.cuda.current_stream())
-    if world > 1:
+    if world > 1 and nccl_usable():
         from paper_1905_09598_b200 import dist as sdist
         sdist.init_nccl(mm.h, rank, world, som.SOM_SHARD_DOCS)
     mm.set_weights(W)
@@ -310,7 +327,7 @@ def c5_leg(som, torch, args, local, rank, world, corpus):
         ms, _, launches = som.som_last_stats(mm.h)
         times.append(ms)
     ms = statistics.mean(times)
-    qe, te = som.som_errors_csr(mm.h, rp, ci, va, n)            # collective at N > 1
+    qe, te = sharded_errors(som, mm.h, rp, ci, va, n, world)    # collective at N > 1
     err_ms = som.som_last_stats(mm.h)[0]
     t = torch.tensor([ms, err_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -455,7 +472,7 @@ def exchange_probe(som, torch, args, local, rank, world):
     X = torch.from_numpy(uniform_matrix(n, 64, args.seed + 700)).cuda(local)
     W0 = torch.from_numpy(uniform_matrix(world * side_c, 64, args.seed + 701)).cuda(local)
     out = {"units_per_gpu": side_c, "d": 64, "steps": steps}
-    for mode in ("mailbox", "nccl"):
+    for mode in ("mailbox", "nccl") if nccl_usable() else ("mailbox",):
         ok = torch.zeros(1, dtype=torch.float64, device="cuda")
         ms = 0.0
         h = None
@@ -673,7 +690,8 @@ def run_b200(args, rank, world, local):
         som.som_set_stream(sm.h, stream)
         md = som.SOM(cfg["rows"], cfg["cols"], d, cfg["topo"], device=local)
         som.som_set_stream(md.h, stream)
-        sdist.init_nccl(md.h, rank, world, som.SOM_SHARD_DOCS)
+        if nccl_usable():
+            sdist.init_nccl(md.h, rank, world, som.SOM_SHARD_DOCS)
         lo, hi = sdist.shard_range(n, rank, world)
         ns = hi - lo
         h_srp = (C.indptr[lo:hi + 1] - C.indptr[lo]).astype(np.int64)
@@ -711,7 +729,7 @@ def run_b200(args, rank, world, local):
             som.som_map_csr(md.h, jrp, jci, jva, ns, ob1, ob2, od1)
             launches += som.som_last_stats(md.h)[2]
             evs[3].record(stream)
-            qe, te = som.som_errors_csr(md.h, jrp, jci, jva, ns)   # NCCL-reduced inside libsom
+            qe, te = sharded_errors(som, md.h, jrp, jci, jva, ns, world)   # NCCL-reduced inside libsom
             launches += som.som_last_stats(md.h)[2]
             evs[4].record(stream)
             som.som_umatrix(md.h, oU)

@@ -78,11 +78,20 @@ typedef enum {
 /* Decay schedule (R1-R6): tau = t/T, alpha_t = alpha0 f,
  * sigma_t = max(sigma_min, sigma0 f); only units with lattice distance^2
  * g2 <= 2 sigma_t^2 ln(1/cutoff) adapt (R5; cutoff = 0: every unit). */
+/* Sample draw of step t ("an input sample is randomly selected"):
+ * SOM_SAMPLE_REPLACE (R8): uniform with replacement, i_t = mulhi64(
+ * SplitMix64 output t of the seed, m); SOM_SAMPLE_PERMUTE (R8b):
+ * a keyed pseudo-random permutation of the m drawable rows per epoch of m
+ * steps (every row exactly once per epoch).  Both are counter-based (no
+ * state crosses calls: t-ranges resume exactly). */
+typedef enum { SOM_SAMPLE_REPLACE = 0, SOM_SAMPLE_PERMUTE = 1 } som_sampling;
+
 typedef struct {
     int32_t kind;      /* som_decay_kind; default SOM_DECAY_GAUSSIAN */
     double k;          /* decay constant; default ln(100)            */
     double sigma_min;  /* radius floor; default 1.0 (R3)              */
     double cutoff;     /* epsilon; default 1e-4 (R5); 0 = no cutoff  */
+    int32_t sampling;  /* som_sampling; default SOM_SAMPLE_REPLACE    */
 } som_schedule;
 
 typedef enum {

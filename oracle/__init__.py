@@ -48,6 +48,8 @@ def lib():
         L.or_splitmix64.argtypes = [u64, i64]
         L.or_sample_index.restype = i64
         L.or_sample_index.argtypes = [u64, i64, i64]
+        L.or_perm_index.restype = i64
+        L.or_perm_index.argtypes = [u64, i64, i64]
         L.or_schedule.restype = None
         L.or_schedule.argtypes = [ctypes.c_int, f64, i64, i64, f64, f64, f64, f64, P, P, P]
         L.or_lattice_g2.restype = f64
@@ -58,10 +60,10 @@ def lib():
         L.or_update.argtypes = [P, i32, i32, i32, i64, P, i64, f64, f64, f64]
         L.or_train_online.restype = ctypes.c_int
         L.or_train_online.argtypes = [P, i32, i32, i32, i64, P, i64, i32, f64, f64, i32,
-                                      f64, f64, f64, u64, i64, i64, P, P]
+                                      f64, f64, f64, i32, u64, i64, i64, P, P]
         L.or_train_online_csr.restype = ctypes.c_int
         L.or_train_online_csr.argtypes = [P, i32, i32, i32, i64, P, P, P, i64, i32, f64, f64, i32,
-                                          f64, f64, f64, u64, i64, i64, P]
+                                          f64, f64, f64, i32, u64, i64, i64, P]
         L.or_map.restype = None
         L.or_map.argtypes = [P, i64, i64, P, i64, P, P, P, P, P]
         L.or_map_csr.restype = None
@@ -110,6 +112,11 @@ def sample_index(seed: int, t: int, n: int) -> int:
     return int(lib().or_sample_index(seed & (2**64 - 1), t, n))
 
 
+def perm_index(seed: int, t: int, m: int) -> int:
+    """R8b: the draw of step t under per-epoch permutation sampling."""
+    return int(lib().or_perm_index(seed & (2**64 - 1), t, m))
+
+
 # ----------------------------------------------------------------- schedule
 def schedule(t, T, alpha0, sigma0, kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0, eps=1e-4):
     a, s, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
@@ -142,7 +149,7 @@ def update(W, rows, cols, topo, x, c, alpha, sigma, r2):
 
 def train_online(W, rows, cols, topo, X, epochs, alpha0, sigma0, seed,
                  kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0, eps=1e-4,
-                 t_begin=0, t_end=-1, want_margins=False):
+                 t_begin=0, t_end=-1, want_margins=False, sampling=0):
     """Online SOM on a copy of W.  Returns (W', bmu_log[, margins])."""
     W = np.array(W, dtype=np.float32, copy=True, order="C")
     X = _f32(X)
@@ -154,7 +161,7 @@ def train_online(W, rows, cols, topo, X, epochs, alpha0, sigma0, seed,
     log = np.empty(steps, dtype=np.int32)
     margins = np.empty(steps, dtype=np.float64) if want_margins else None
     rc = lib().or_train_online(_p(W), rows, cols, topo, d, _p(X), n, epochs, alpha0, sigma0,
-                               kind, k, sigma_min, eps, seed & (2**64 - 1), t_begin, te,
+                               kind, k, sigma_min, eps, sampling, seed & (2**64 - 1), t_begin, te,
                                _p(log), _p(margins))
     if rc == -2:
         raise ValueError("or_train_online: EmptyData (every row is zero, S:219)")
@@ -164,7 +171,7 @@ def train_online(W, rows, cols, topo, X, epochs, alpha0, sigma0, seed,
 
 
 def train_online_csr(W, rows, cols, topo, rowptr, col, val, epochs, alpha0, sigma0, seed,
-                     kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0, eps=1e-4, t_begin=0, t_end=-1):
+                     kind=DECAY_GAUSSIAN, k=LN100, sigma_min=1.0, eps=1e-4, t_begin=0, t_end=-1, sampling=0):
     """Online SOM on CSR rows (x_t densified per step).  Returns (W', bmu_log)."""
     W = np.array(W, dtype=np.float32, copy=True, order="C")
     rowptr = np.ascontiguousarray(rowptr, np.int64)
@@ -176,7 +183,8 @@ def train_online_csr(W, rows, cols, topo, rowptr, col, val, epochs, alpha0, sigm
     te = T if t_end < 0 else t_end
     log = np.empty(max(te - t_begin, 0), dtype=np.int32)
     rc = lib().or_train_online_csr(_p(W), rows, cols, topo, d, _p(rowptr), _p(col), _p(val), n, epochs, alpha0,
-                                   sigma0, kind, k, sigma_min, eps, seed & (2**64 - 1), t_begin, te, _p(log))
+                                   sigma0, kind, k, sigma_min, eps, sampling, seed & (2**64 - 1), t_begin, te,
+                                   _p(log))
     if rc == -2:
         raise ValueError("or_train_online_csr: EmptyData (every row is zero, S:219)")
     if rc != 0:

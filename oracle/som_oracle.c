@@ -52,6 +52,39 @@ int64_t or_sample_index(uint64_t seed, int64_t t, int64_t n)
     return (int64_t)(p >> 64);
 }
 
+/* R8b (per-epoch permutation as an option to R8): epoch
+ * e = t / m, position p = t mod m, i_t = pi_e(p) with pi_e the permutation
+ * of [0, m) obtained by cycle-walking a keyed bijection of [0, 2^b),
+ * b = bit length of m - 1: four rounds of (add key r, xor with itself
+ * shifted right by ceil(b/2), multiply by 0x9E3779B97F4A7C15), every
+ * operation mod 2^b, keys k_r = or_splitmix64(seed ^ 0x5851F42D4C957F2D,
+ * 4e + r).  Every index appears exactly once per epoch. */
+int64_t or_perm_index(uint64_t seed, int64_t t, int64_t m)
+{
+    if (m <= 1) return 0;
+    int64_t e = t / m, p = t % m;
+    int b = 64 - __builtin_clzll((uint64_t)(m - 1));
+    uint64_t mask = b >= 64 ? ~0ULL : ((1ULL << b) - 1ULL);
+    int sh = (b + 1) / 2;
+    uint64_t k[4];
+    for (int r = 0; r < 4; ++r) k[r] = or_splitmix64(seed ^ 0x5851F42D4C957F2DULL, 4 * e + r);
+    uint64_t x = (uint64_t)p;
+    do {
+        for (int r = 0; r < 4; ++r) {
+            x = (x + k[r]) & mask;
+            x ^= x >> sh;
+            x = (x * 0x9E3779B97F4A7C15ULL) & mask;
+        }
+    } while (x >= (uint64_t)m);
+    return (int64_t)x;
+}
+
+/* the draw of step t over m drawable rows: R8 (sampling 0) or R8b (1) */
+int64_t or_draw_index(uint64_t seed, int64_t t, int64_t m, int32_t sampling)
+{
+    return sampling == 1 ? or_perm_index(seed, t, m) : or_sample_index(seed, t, m);
+}
+
 /* --------------------------------------------------------------- schedule */
 /* R1 ("The Gaussian decay was used to smooth the learning rate and
  * neighborhood radius"): tau = t/T, f = exp(-k tau^2);
@@ -199,13 +232,13 @@ int64_t or_nonzero_rows_csr(const int64_t *rowptr, const float *val, int64_t n, 
 int or_train_online(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t d,
                     const float *X, int64_t n, int32_t epochs,
                     double alpha0, double sigma0, int32_t decay_kind, double k,
-                    double sigma_min, double eps, uint64_t seed,
+                    double sigma_min, double eps, int32_t sampling, uint64_t seed,
                     int64_t t_begin, int64_t t_end,
                     int32_t *bmu_log, double *margin_log)
 {
     int64_t T = (int64_t)epochs * n;
     if (t_end < 0) t_end = T;
-    if (t_begin < 0 || t_begin > t_end || t_end > T) return -1;
+    if (t_begin < 0 || t_begin > t_end || t_end > T || sampling < 0 || sampling > 1) return -1;
     if (t_end == t_begin) return 0;
     int64_t N = (int64_t)rows * cols;
     /* R8 + S:218: draws are uniform over the non-zero rows only (the j-th
@@ -216,7 +249,7 @@ int or_train_online(float *W, int32_t rows, int32_t cols, int32_t topo, int64_t 
     int64_t m = or_nonzero_rows(X, n, d, nzr);
     if (m == 0) { free(nzr); return -2; }   /* EmptyData */
     for (int64_t t = t_begin; t < t_end; ++t) {
-        int64_t i = nzr[or_sample_index(seed, t, m)];
+        int64_t i = nzr[or_draw_index(seed, t, m, sampling)];
         const float *x = X + i * d;
         double margin;
         int64_t c = or_bmu(W, N, d, x, NULL, &margin);
@@ -239,11 +272,11 @@ int or_train_online_csr(float *W, int32_t rows, int32_t cols, int32_t topo, int6
                         const int64_t *rowptr, const int32_t *col, const float *val,
                         int64_t n, int32_t epochs, double alpha0, double sigma0,
                         int32_t decay_kind, double k, double sigma_min, double eps,
-                        uint64_t seed, int64_t t_begin, int64_t t_end, int32_t *bmu_log)
+                        int32_t sampling, uint64_t seed, int64_t t_begin, int64_t t_end, int32_t *bmu_log)
 {
     int64_t T = (int64_t)epochs * n;
     if (t_end < 0) t_end = T;
-    if (t_begin < 0 || t_begin > t_end || t_end > T) return -1;
+    if (t_begin < 0 || t_begin > t_end || t_end > T || sampling < 0 || sampling > 1) return -1;
     if (t_end == t_begin) return 0;
     int64_t N = (int64_t)rows * cols;
     int64_t *nzr = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
@@ -252,7 +285,7 @@ int or_train_online_csr(float *W, int32_t rows, int32_t cols, int32_t topo, int6
     int64_t m = or_nonzero_rows_csr(rowptr, val, n, nzr);
     if (m == 0) { free(nzr); free(x); return -2; }
     for (int64_t t = t_begin; t < t_end; ++t) {
-        int64_t i = nzr[or_sample_index(seed, t, m)];
+        int64_t i = nzr[or_draw_index(seed, t, m, sampling)];
         for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) x[col[p]] = val[p];
         int64_t c = or_bmu(W, N, d, x, NULL, NULL);
         double alpha, sigma, r2;

@@ -168,6 +168,7 @@ som_status som_schedule_default(som_schedule* s) {
     s->k = std::log(100.0);
     s->sigma_min = 1.0;
     s->cutoff = 1e-4;
+    s->sampling = SOM_SAMPLE_REPLACE;
     return SOM_OK;
 }
 

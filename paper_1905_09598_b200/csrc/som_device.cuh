@@ -20,6 +20,31 @@ __device__ __forceinline__ int64_t sample_at(uint64_t seed, int64_t t, int64_t n
     return (int64_t)__umul64hi(splitmix64_at(seed, t), (uint64_t)n);
 }
 
+// R8b (optional per-epoch permutation): epoch e = t / m, position p = t mod
+// m; cycle-walk a keyed bijection of [0, 2^b) (b = bit length of m - 1):
+// four rounds of add key, xor-shift right by ceil(b/2), multiply by an odd
+// constant, all mod 2^b; keys = SplitMix64 outputs 4e + r of a derived seed.
+__device__ __forceinline__ int64_t perm_at(uint64_t seed, int64_t t, int64_t m) {
+    if (m <= 1) return 0;
+    const int64_t e = t / m, p = t - e * m;
+    const int b = 64 - __clzll((long long)(m - 1));
+    const uint64_t mask = b >= 64 ? ~0ull : ((1ull << b) - 1ull);
+    const int sh = (b + 1) / 2;
+    uint64_t k[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) k[r] = splitmix64_at(seed ^ 0x5851F42D4C957F2DULL, 4 * e + r);
+    uint64_t x = (uint64_t)p;
+    do {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            x = (x + k[r]) & mask;
+            x ^= x >> sh;
+            x = (x * 0x9E3779B97F4A7C15ULL) & mask;
+        }
+    } while (x >= (uint64_t)m);
+    return (int64_t)x;
+}
+
 // P:166 / S:164: squared lattice distance, exact (multiples of 1/4).
 // rect: di^2 + dj^2; hex (pointy-top, odd rows shifted right by 1/2):
 // (dj + ((iu&1) - (iv&1))/2)^2 + 3/4 di^2.

@@ -36,6 +36,7 @@ struct TrainArgs {
     // row, draws uniform over [0, n)
     const int64_t* rowmap;
     int64_t n_draw;
+    int sampling;              // 0: R8 (uniform with replacement), 1: R8b (per-epoch permutation)
     double alpha0, sigma0, sigma_min, ln_inv_eps;
     int cutoff_on;             // 0: every unit adapts (eps = 0)
     unsigned long long* xchg;  // [2][G] per-CTA BMU candidate slots
@@ -167,8 +168,9 @@ inline cudaError_t launch_persistent(const void* fn, const TrainArgs& a, int thr
 
 // R8 + S:218: the row drawn at step t (uniform over the non-zero rows)
 __device__ __forceinline__ int64_t train_row(const TrainArgs& a, int64_t t) {
-    if (a.rowmap) return __ldg(a.rowmap + sample_at(a.seed, t, a.n_draw));
-    return sample_at(a.seed, t, a.n);
+    const int64_t m = a.rowmap ? a.n_draw : a.n;
+    const int64_t j = a.sampling == 1 ? perm_at(a.seed, t, m) : sample_at(a.seed, t, m);
+    return a.rowmap ? __ldg(a.rowmap + j) : j;
 }
 
 // global unit index of local unit l

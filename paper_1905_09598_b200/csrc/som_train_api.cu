@@ -20,6 +20,7 @@ som_status check_train(som_ctx* h, int64_t n, int32_t epochs, double alpha0, dou
     if (!(alpha0 >= 0.0 && alpha0 <= 1.0)) return fail(SOM_EINVAL, "alpha0 must be in [0, 1]");
     if (!(sigma0 > 0.0) || !std::isfinite(sigma0)) return fail(SOM_EINVAL, "sigma0 must be > 0");
     if (sd->kind < 0 || sd->kind > 2) return fail(SOM_EINVAL, "unknown decay kind");
+    if (sd->sampling < 0 || sd->sampling > 1) return fail(SOM_EINVAL, "unknown sampling mode");
     if (!(sd->k > 0.0) || !std::isfinite(sd->k)) return fail(SOM_EINVAL, "decay constant k must be > 0");
     if (!(sd->sigma_min > 0.0)) return fail(SOM_EINVAL, "sigma_min must be > 0");
     if (!(sd->cutoff >= 0.0 && sd->cutoff < 1.0)) return fail(SOM_EINVAL, "cutoff must be in [0, 1)");
@@ -87,7 +88,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
 
     TrainArgs a{};
     a.W = h->W; a.X = (const float*)Xd; a.n = n; a.dim = h->dim; a.dimp = (h->dim + 3) & ~3;
-    a.rowmap = rowmap; a.n_draw = n_draw;
+    a.rowmap = rowmap; a.n_draw = n_draw; a.sampling = sd.sampling;
     a.rows = h->rows; a.cols = h->cols; a.topo = h->topo; a.N = h->NL;
     a.rank = h->rank; a.world = h->world;
     for (int p = 0; p < kMaxRanks; ++p) a.mail[p] = h->peer_mail[p];

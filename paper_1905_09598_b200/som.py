@@ -24,6 +24,7 @@ SOM_MAP_AUTO, SOM_MAP_EXACT_F64, SOM_MAP_3XTF32, SOM_MAP_SPARSE_F64 = 0, 1, 2, 3
 SOM_TRAIN_AUTO, SOM_TRAIN_W_SHARED, SOM_TRAIN_W_GLOBAL, SOM_TRAIN_W_REGISTERS = 0, 1, 2, 3
 SOM_SHARD_DOCS, SOM_SHARD_NEURONS = 1, 2
 SOM_XCHG_MAILBOX, SOM_XCHG_NCCL = 0, 1
+SOM_SAMPLE_REPLACE, SOM_SAMPLE_PERMUTE = 0, 1
 
 _STATUS = {0: "SOM_OK", 1: "SOM_EINVAL", 2: "SOM_EDIM", 3: "SOM_EEMPTY", 4: "SOM_ENOMEM", 5: "SOM_ECUDA",
            6: "SOM_ENCCL", 7: "SOM_ESTATE", 8: "SOM_EUNSUPPORTED"}
@@ -37,7 +38,7 @@ class SomError(RuntimeError):
 
 class som_schedule(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("k", ctypes.c_double), ("sigma_min", ctypes.c_double),
-                ("cutoff", ctypes.c_double)]
+                ("cutoff", ctypes.c_double), ("sampling", ctypes.c_int32)]
 
 
 _lib = None
@@ -533,20 +534,21 @@ class SOM:
 
     def train_online(self, X, epochs: int, alpha0: float = 0.1, sigma0: float | None = None, seed: int = 1,
                      kind: int = SOM_DECAY_GAUSSIAN, k: float = math.log(100.0), sigma_min: float = 1.0,
-                     cutoff: float = 1e-4, t_begin: int = 0, t_end: int = -1, bmu_log=None):
+                     cutoff: float = 1e-4, t_begin: int = 0, t_end: int = -1, bmu_log=None,
+                     sampling: int = SOM_SAMPLE_REPLACE):
         if sigma0 is None:
             sigma0 = max(self.rows, self.cols) / 2.0
-        s = som_schedule(kind, k, sigma_min, cutoff)
+        s = som_schedule(kind, k, sigma_min, cutoff, sampling)
         som_train_online(self.h, X, X.shape[0], epochs, alpha0, sigma0, s, seed, t_begin, t_end, bmu_log)
         return bmu_log
 
     def train_online_csr(self, rowptr, col, val, n: int, epochs: int, alpha0: float = 0.1,
                          sigma0: float | None = None, seed: int = 1, kind: int = SOM_DECAY_GAUSSIAN,
                          k: float = math.log(100.0), sigma_min: float = 1.0, cutoff: float = 1e-4,
-                         t_begin: int = 0, t_end: int = -1, bmu_log=None):
+                         t_begin: int = 0, t_end: int = -1, bmu_log=None, sampling: int = SOM_SAMPLE_REPLACE):
         if sigma0 is None:
             sigma0 = max(self.rows, self.cols) / 2.0
-        s = som_schedule(kind, k, sigma_min, cutoff)
+        s = som_schedule(kind, k, sigma_min, cutoff, sampling)
         som_train_online_csr(self.h, rowptr, col, val, n, epochs, alpha0, sigma0, s, seed, t_begin, t_end, bmu_log)
         return bmu_log
 

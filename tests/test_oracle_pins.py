@@ -554,3 +554,50 @@ def test_csr_training_equals_dense_training():
     Wa, la = oracle.train_online(W0, 4, 4, 1, X, epochs=2, alpha0=0.2, sigma0=2.0, seed=6)
     Wb, lb = oracle.train_online_csr(W0, 4, 4, 1, rp, ci, va, epochs=2, alpha0=0.2, sigma0=2.0, seed=6)
     assert np.array_equal(Wa, Wb) and np.array_equal(la, lb)
+
+
+def test_permutation_sampler_is_a_permutation_per_epoch():
+    """R8b (per-epoch permutation option of P:162's random
+    selection): within each epoch of m steps every index of [0, m) is drawn
+    exactly once (brute force over several m, including powers of two and
+    their neighbours, where the cycle-walking domain is tight or loose), and
+    consecutive epochs use different orders."""
+    for m in (1, 2, 3, 4, 5, 7, 8, 9, 31, 32, 33, 100, 1000, 5000):
+        orders = []
+        for e in range(3):
+            draws = [oracle.perm_index(42, e * m + p, m) for p in range(m)]
+            assert sorted(draws) == list(range(m)), (m, e)
+            orders.append(draws)
+        if m >= 5:
+            assert orders[0] != orders[1] and orders[1] != orders[2]
+    # seed-dependence and counter-based resume: the same t gives the same draw
+    assert [oracle.perm_index(1, t, 100) for t in range(100)] != [oracle.perm_index(2, t, 100) for t in range(100)]
+    assert oracle.perm_index(7, 12345, 5000) == oracle.perm_index(7, 12345, 5000)
+
+
+def test_permutation_sampling_training_draws_every_row_once():
+    """Online training with R8b on a 1x1 map: the single prototype's
+    trajectory w <- fmaf(h, RN32(x - w), w) (Eq. 1, R11; h = RN32(alpha_t)
+    since g2 = 0) is replayed by hand along the draws perm_index gives over
+    the non-zero rows (zero rows are never drawn); the first epoch
+    draws every non-zero row once."""
+    rng = np.random.default_rng(3)
+    X = rng.random((9, 4)).astype(np.float32)
+    X[[2, 5]] = 0.0                       # zero rows: drawable rows m = 7
+    nz = [i for i in range(9) if X[i].any()]
+    draws = [nz[oracle.perm_index(11, t, len(nz))] for t in range(len(nz))]
+    assert sorted(draws) == nz
+    # the oracle's training with sampling=1 follows exactly these draws: with
+    # a 1x1 map and eps = 0 the prototype after step t is
+    # fmaf(alpha_t, x - w, w), so replay it here with the same arithmetic
+    W0 = np.zeros((1, 4), np.float32)
+    W, log = oracle.train_online(W0, 1, 1, 0, X, 1, 0.5, 1.0, 11, eps=0.0, sampling=1)
+    T = X.shape[0]                    # T = epochs * n steps (R7); epochs of R8b are m = 7 steps
+    w = W0[0].astype(np.float64)
+    for t in range(T):
+        a, _, _ = oracle.schedule(t, T, 0.5, 1.0, eps=0.0)
+        h = float(np.float32(a))      # g2 = 0: h = RN32(alpha) (R4)
+        x = X[nz[oracle.perm_index(11, t, len(nz))]].astype(np.float64)
+        diff = (x.astype(np.float32) - w.astype(np.float32)).astype(np.float64)   # RN32(x - w) (R11)
+        w = np.float32(h * diff + w).astype(np.float64)   # fmaf: one rounding of the exact h*diff + w
+    assert np.array_equal(W[0], w.astype(np.float32))
