@@ -356,6 +356,7 @@ def c5_leg(som, torch, args, local, rank, world, corpus):
         som.som_map_csr(mm.h, rp, ci, va, ns, b1, b2, d1)
         tc_ms.append(som.som_last_stats(mm.h)[0])
     tcm = statistics.mean(tc_ms)
+    tc_fallbacks = som.som_last_map_fallbacks(mm.h)
     mm.close()
     nnz = float(val.size)
     work = nnz * N                                               # conversions + FMAs (one per non-zero per unit)
@@ -389,10 +390,14 @@ def c5_leg(som, torch, args, local, rank, world, corpus):
                          "work": "nnz x N fp32->fp64 conversions + fp64 FMAs per call (incl. the top-2 merge)"},
             "cpu_baseline": cpu,
             "tc_3xtf32": {"docs": ns, "docs_per_s": ns / (tcm / 1e3), "ms": tcm,
+                          "exact_fallback_docs": tc_fallbacks,
+                          "what": "3xTF32 candidates (4 per document) rescored by the exact fp64 definition and "
+                                  "certified (R20b): bmu1/bmu2/D1 exact for every document",
                           "roofline": {"bound": "tensor", "kernel": "map_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
                                        "achieved": executed, "peak": tpeak, "unit": "TFLOP/s",
                                        "frac": executed / tpeak, "peak_source": tsrc,
-                                       "work": "3 x 2 n N d executed TF32 flop per call, incl. split + merge"}}}
+                                       "work": "3 x 2 n N d executed TF32 flop per call over the whole call "
+                                               "(split, GEMM, certified rescoring)"}}}
 
 
 def c4_leg(som, torch, args, local, rank, world):

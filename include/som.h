@@ -211,6 +211,12 @@ som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
  * exact fallback pass (0 for other kernels).  *count >= 0. */
 som_status som_last_spec_fallbacks(som_ctx *h, int64_t *count);
 
+/* SOM_MAP_3XTF32 only (R20b): number of documents of the last mapping call
+ * whose 4 tensor-core candidates could not be certified and that were mapped
+ * by the exact definition over every unit instead (0 after other paths).
+ * Every document's bmu1 / bmu2 / D1 are exact either way. */
+som_status som_last_map_fallbacks(som_ctx *h, int64_t *count);
+
 /* ---- Neuron sharding: online training of one map across
  * `world` GPUs (one process or handle per rank).  Rank r holds the units
  * u = r + world*l (cyclic, so the shrinking neighbourhood stays spread);

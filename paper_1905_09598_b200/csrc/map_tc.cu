@@ -6,9 +6,17 @@
 // x . w is a true documents x units x vocabulary contraction, run as
 // 3xTF32: x = x_hi + x_lo, w = w_hi + w_lo with hi = cvt.rna.tf32(v),
 // lo = cvt.rna.tf32(v - hi) (split once, in global memory, by split_kernel),
-// and x.w ~ x_lo.w_hi + x_hi.w_lo + x_hi.w_hi accumulated in fp32 in TMEM
-// (error ~1e-7 relative, far inside the 1e-5 near-tie margin, R19).  Norms
-// are summed in fp64 by the split kernel.
+// and x.w ~ x_lo.w_hi + x_hi.w_lo + x_hi.w_hi accumulated in fp32 in TMEM;
+// norms are summed in fp64 by the split kernels and D is formed in fp64.
+// The GEMM is a filter (R20b): its epilogue keeps the 4 smallest approximate
+// D per document and unit tile, a merge keeps the 4 smallest overall, and a
+// rescoring kernel computes the exact fp64 D (the dense definition, R10) of
+// those candidates and certifies the result against a bound E on the
+// approximation error: every other unit has exact D >= (4th approximate D) -
+// E; if that exceeds the 2nd exact candidate by more than an fp32 ulp, the
+// exact top-2 are among the candidates, else the document is mapped exactly
+// over all units in the same kernel.  bmu1, bmu2 and D1 are therefore those
+// of the exact definition for every document.
 //
 // Kernel: persistent CTAs of 6 warps.  warp 0 = TMA producer (4 tiles per
 // K-block: A_hi, A_lo 128x32 fp32, B_hi, B_lo BNx32 fp32, 128B swizzle),
@@ -39,6 +47,7 @@ constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;            // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;            // 32 KB
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
 constexpr uint32_t TMEM_COLS = 2 * TC_BN;                  // hh and lo accumulators
+constexpr int TC_K = 4;                                    // candidates per document (R20b)
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -128,9 +137,9 @@ struct TcArgs {
     int n_tiles;      // ceil(N / BN)
     int m_blocks;     // ceil(n / 128)
     int group;        // unit tiles per raster group (L2 reuse of A and B panels)
-    const float* xnorm;   // [n] fp32 of the fp64 |x|^2
-    const float* wnorm;   // [N] fp32 of the fp64 |w|^2
-    unsigned long long* keys;   // [n_tiles][n][2] partial top-2 per unit tile
+    const double* xnorm;  // [n] fp64 |x|^2
+    const double* wnorm;  // [N] fp64 |w|^2
+    unsigned long long* keys;   // [n_tiles][n][TC_K] partial top-K per unit tile
 };
 
 // Work item wi -> (document block, unit tile).  Grouped raster: unit tiles
@@ -250,9 +259,10 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
             int mb, nt;
             work_coords(wi, a, mb, nt);
             const int64_t row = (int64_t)mb * TC_BM + row_in_tile;
-            const float xn = row < a.n ? a.xnorm[row] : 0.0f;
-            float d1 = INFINITY, d2 = INFINITY;
-            int u1 = -1, u2 = -1;
+            const double xn = row < a.n ? a.xnorm[row] : 0.0;
+            unsigned long long kk[TC_K];
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) kk[j] = ~0ull;
             {
                 const uint32_t buf = 0, tph = tile & 1;
                 mbar_wait(&tfull[buf], tph);
@@ -263,18 +273,24 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
                     float v[32], vl[32];
                     tmem_ld32(taddr + c * 32, v);
                     tmem_ld32(taddr + TC_BN + c * 32, vl);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] += vl[i];
                     const int u0 = nt * TC_BN + c * 32;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int u = u0 + i;
                         if (u < a.N) {
-                            // D = |x|^2 + |w|^2 - 2 x.w, clamped >= 0 (R20)
-                            float D = fmaf(-2.0f, v[i], xn + __ldg(a.wnorm + u));
-                            D = fmaxf(D, 0.0f);
-                            if (D < d1) { d2 = d1; u2 = u1; d1 = D; u1 = u; }
-                            else if (D < d2) { d2 = D; u2 = u; }
+                            // D = |x|^2 + |w|^2 - 2 x.w in fp64 from the two
+                            // fp32 accumulators, clamped >= 0 (R20), rounded
+                            // to fp32 for the candidate key
+                            const double xw = (double)v[i] + (double)vl[i];
+                            const double D = fmax(fma(-2.0, xw, xn + __ldg(a.wnorm + u)), 0.0);
+                            unsigned long long k = make_key((float)D, u);
+                            // insertion into the sorted top-K
+#pragma unroll
+                            for (int j = 0; j < TC_K; ++j) {
+                                const unsigned long long lo = umin64(kk[j], k), hi = kk[j] < k ? k : kk[j];
+                                kk[j] = lo;
+                                k = hi;
+                            }
                         }
                     }
                 }
@@ -283,9 +299,9 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
                 if (lane == 0) mbar_arrive(&tempty[buf]);
             }
             if (row < a.n) {
-                unsigned long long* dst = a.keys + ((size_t)nt * a.n + row) * 2;
-                dst[0] = u1 >= 0 ? make_key(d1, u1) : ~0ull;
-                dst[1] = u2 >= 0 ? make_key(d2, u2) : ~0ull;
+                unsigned long long* dst = a.keys + ((size_t)nt * a.n + row) * TC_K;
+#pragma unroll
+                for (int j = 0; j < TC_K; ++j) dst[j] = kk[j];
             }
         }
     }
@@ -294,10 +310,12 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
 }
 
 // Split rows of a dense fp32 matrix into tf32 hi / lo parts (K padded to a
-// multiple of 32 with zeros) and the fp64 squared norm of each row, rounded
-// to fp32.  One warp per row; fixed reduction order (deterministic).
+// multiple of 32 with zeros), the fp64 squared norm of each row and (groups,
+// nullable) the number of 8-wide K groups holding a non-zero (the MMA steps
+// whose accumulation can round, R20b).  One warp per row; fixed reduction
+// order (deterministic).
 __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int d, int dp, float* __restrict__ hi,
-                             float* __restrict__ lo, float* __restrict__ norm) {
+                             float* __restrict__ lo, double* __restrict__ norm, int* __restrict__ groups) {
     const int lane = threadIdx.x & 31;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -306,6 +324,7 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int d,
         float* h = hi + r * dp;
         float* l = lo + r * dp;
         double acc = 0.0;
+        int g = 0;
         for (int k = lane; k < dp; k += 32) {
             const float v = k < d ? s[k] : 0.0f;
             uint32_t hb;
@@ -316,16 +335,23 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int d,
             h[k] = hv;
             l[k] = __uint_as_float(lb);
             acc = fma((double)v, (double)v, acc);
+            // lanes 8q..8q+7 hold one K group of this 32-wide slab
+            const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0f);
+            if (lane == 0) g += ((nzm & 0xFFu) != 0u) + ((nzm & 0xFF00u) != 0u) + ((nzm & 0xFF0000u) != 0u) +
+                                ((nzm & 0xFF000000u) != 0u);
         }
         acc = warp_sum_f64(acc);
-        if (lane == 0) norm[r] = (float)acc;
+        if (lane == 0) {
+            norm[r] = acc;
+            if (groups) groups[r] = g;
+        }
     }
 }
 
 // CSR rows -> split dense rows (zero + scatter) and norms from the non-zeros.
 __global__ void split_csr_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                  const float* __restrict__ val, int64_t r0, int64_t rows, int dp, float* __restrict__ hi,
-                                 float* __restrict__ lo, float* __restrict__ norm) {
+                                 float* __restrict__ lo, double* __restrict__ norm, int* __restrict__ groups) {
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         float* h = hi + r * dp;
         float* l = lo + r * dp;
@@ -333,6 +359,9 @@ __global__ void split_csr_kernel(const int64_t* __restrict__ rowptr, const int32
         __syncthreads();
         const int64_t p0 = rowptr[r0 + r], p1 = rowptr[r0 + r + 1];
         double acc = 0.0;
+        int g = 0;   // distinct K groups (col >> 3) among the sorted columns
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x)
+            g += (p == p0 || (col[p] >> 3) != (col[p - 1] >> 3));
         for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
             const float v = val[p];
             uint32_t hb, lb;
@@ -345,15 +374,309 @@ __global__ void split_csr_kernel(const int64_t* __restrict__ rowptr, const int32
         }
         // block reduction (fixed order)
         __shared__ double red[32];
+        __shared__ int gred[32];
         acc = warp_sum_f64(acc);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+        if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = acc; gred[threadIdx.x >> 5] = g; }
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-            norm[r] = (float)t;
+            int gt = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red[w]; gt += gred[w]; }
+            norm[r] = t;
+            if (groups) groups[r] = gt;
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------ certified rescoring (R20b)
+// x_i for the rescoring: CSR rows (rowptr/col/val from row r0) or dense rows X
+struct XSrc {
+    const int64_t* rowptr;
+    const int32_t* col;
+    const float* val;
+    int64_t r0;
+    const float* X;
+};
+
+__device__ __forceinline__ void top_insert(unsigned long long (&kk)[TC_K], unsigned long long k) {
+#pragma unroll
+    for (int j = 0; j < TC_K; ++j) {
+        const unsigned long long lo = umin64(kk[j], k), hi = kk[j] < k ? k : kk[j];
+        kk[j] = lo;
+        k = hi;
+    }
+}
+
+constexpr int RS_THREADS = 256;   // two CTAs (two documents in flight) per SM
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+// Block-wide exact fp64 D (the dense definition, R10) of up to TC_K units
+// (u < 0: skipped) against the document in shared memory; fixed summation
+// order (per thread, warp butterfly, warps in order); result in out[] on
+// thread 0.  Loads unrolled 4 x TC_K deep (latency).
+__device__ __forceinline__ void exact_k(const float* xs, const float* __restrict__ W, int d, const int (&cu)[TC_K],
+                                        double (*part)[TC_K], double (&out)[TC_K]) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc[TC_K];
+#pragma unroll
+    for (int j = 0; j < TC_K; ++j) acc[j] = 0.0;
+    int k = tid;
+    for (; k + 3 * RS_THREADS < d; k += 4 * RS_THREADS) {
+        float wv[4][TC_K];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j)
+                wv[q][j] = cu[j] >= 0 ? __ldg(W + (int64_t)cu[j] * d + k + q * RS_THREADS) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double xv = (double)xs[k + q * RS_THREADS];
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) {
+                const double e = xv - (double)wv[q][j];
+                acc[j] = fma(e, e, acc[j]);
+            }
+        }
+    }
+    for (; k < d; k += RS_THREADS) {
+        const double xv = (double)xs[k];
+#pragma unroll
+        for (int j = 0; j < TC_K; ++j) {
+            if (cu[j] < 0) continue;
+            const double e = xv - (double)__ldg(W + (int64_t)cu[j] * d + k);
+            acc[j] = fma(e, e, acc[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < TC_K; ++j) {
+        const double v = warp_sum_f64(acc[j]);
+        if (lane == 0) part[warp][j] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+        for (int j = 0; j < TC_K; ++j) {
+            double t = 0.0;
+            for (int w = 0; w < RS_WARPS; ++w) t += part[w][j];
+            out[j] = t;
+        }
+    }
+}
+
+// Certificate (thread 0): candidates c[] with exact fp64 D exd[]; every
+// other unit has exact D >= lb.  True: (e1, e2) = the exact top-2 (R9 keys).
+__device__ __forceinline__ bool certify(const int (&cu)[TC_K], const double (&exd)[TC_K], double lb, int N,
+                                        unsigned long long& e1, unsigned long long& e2) {
+    e1 = e2 = ~0ull;
+    int nv = 0;
+#pragma unroll
+    for (int j = 0; j < TC_K; ++j) {
+        if (cu[j] < 0) continue;
+        ++nv;
+        const unsigned long long k = make_key((float)exd[j], cu[j]);
+        if (k < e1) { e2 = e1; e1 = k; } else if (k < e2) e2 = k;
+    }
+    if (nv >= N) return true;                 // every unit is a candidate
+    if (nv < TC_K || e2 == ~0ull) return false;
+    // every other unit's RN32(D) >= RN32(lb) > fp32 D of the 2nd candidate:
+    // no unit outside can come before it, not even on an fp32 tie (R9)
+    return lb > (double)nextafterf(key_dist(e2), INFINITY);
+}
+
+// One CTA per document: merge the per-tile candidates, exact fp64 D of the
+// 4 candidates (dense definition, R10), certificate; else (rare) the sparse
+// identity (R25) over every unit picks 4 new candidates certified with R25's
+// own error bound; else the dense definition over every unit.
+// d2 = RN32(exact D of bmu1).
+__global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(
+    const unsigned long long* __restrict__ keys, int n_tiles, int64_t n, const XSrc xs_src, const float* __restrict__ W,
+    int N, int d, const double* __restrict__ xnorm, const double* __restrict__ wnorm, const int* __restrict__ groups,
+    const double* __restrict__ wmax_p, int32_t* __restrict__ bmu1, int32_t* __restrict__ bmu2, float* __restrict__ d2,
+    int* __restrict__ nfall) {
+    extern __shared__ __align__(16) float xs[];          // the document, dense (d floats)
+    __shared__ unsigned long long cand[TC_K];
+    __shared__ unsigned long long wtop[RS_WARPS][TC_K];
+    __shared__ double part[RS_WARPS][TC_K];
+    __shared__ int s_ok;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double wmax = *wmax_p;
+    // block merge of per-thread top-K lists -> cand[] (all threads call)
+    auto block_topk = [&](unsigned long long (&kk)[TC_K]) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long other[TC_K];
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) other[j] = __shfl_xor_sync(0xffffffffu, kk[j], o);
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) top_insert(kk, other[j]);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) wtop[warp][j] = kk[j];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t[TC_K];
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) t[j] = ~0ull;
+            for (int w = 0; w < RS_WARPS; ++w)
+#pragma unroll
+                for (int j = 0; j < TC_K; ++j) top_insert(t, wtop[w][j]);
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) cand[j] = t[j];
+        }
+        __syncthreads();
+    };
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        // the document -> shared memory (dense)
+        if (xs_src.X) {
+            const float* xr = xs_src.X + i * (int64_t)d;
+            for (int k = tid; k < d; k += RS_THREADS) xs[k] = xr[k];
+        } else {
+            for (int k = tid; k < d; k += RS_THREADS) xs[k] = 0.0f;
+            __syncthreads();
+            const int64_t p0 = xs_src.rowptr[xs_src.r0 + i], p1 = xs_src.rowptr[xs_src.r0 + i + 1];
+            for (int64_t p = p0 + tid; p < p1; p += RS_THREADS) xs[xs_src.col[p]] = xs_src.val[p];
+        }
+        // candidates of the 3xTF32 filter: top-K over the unit tiles
+        {
+            unsigned long long kk[TC_K];
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) kk[j] = ~0ull;
+            for (int t = tid; t < n_tiles; t += RS_THREADS) {
+                const unsigned long long* p = keys + ((size_t)t * n + i) * TC_K;
+#pragma unroll
+                for (int j = 0; j < TC_K; ++j) top_insert(kk, p[j]);
+            }
+            block_topk(kk);   // (its barrier also publishes xs)
+        }
+        int cu[TC_K];
+#pragma unroll
+        for (int j = 0; j < TC_K; ++j) cu[j] = cand[j] == ~0ull ? -1 : key_unit(cand[j]);
+        double exd[TC_K];
+        exact_k(xs, W, d, cu, part, exd);
+        const double xn = xnorm[i];
+        if (tid == 0) {
+            // every other unit v: approximate D >= float(A_K) - ulp, exact
+            // D >= that - E, E = 2 (g + 2) 2^-20 |x| max|w| (+ fp64 slop)
+            const double E = 2.0 * ((double)groups[i] + 2.0) * 0x1p-20 * sqrt(xn) * wmax + 1e-14 * (xn + wmax * wmax);
+            const double lb = cand[TC_K - 1] == ~0ull ? INFINITY
+                                                      : (double)nextafterf(key_dist(cand[TC_K - 1]), -INFINITY) - E;
+            unsigned long long e1, e2;
+            const bool ok = certify(cu, exd, lb, N, e1, e2);
+            if (ok) {
+                bmu1[i] = key_unit(e1);
+                if (bmu2) bmu2[i] = e2 == ~0ull ? -1 : key_unit(e2);
+                if (d2) d2[i] = key_dist(e1);
+            } else {
+                atomicAdd(nfall, 1);
+            }
+            s_ok = ok ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_ok) continue;
+        // ---- fallback A (CSR documents): the sparse identity over every
+        // unit (R25), D_u = |w_u|^2 + sum_{k in nz(x)} ((x_k - w_uk)^2 -
+        // w_uk^2), thread per unit; its error is <= (d + nnz + 8) 2^-52
+        // (|x|^2 + max|w|^2) (fp64 sums of exact products), so its top-K are
+        // certified by the same rule after exact rescoring
+        if (!xs_src.X) {
+            const int64_t p0 = xs_src.rowptr[xs_src.r0 + i], p1 = xs_src.rowptr[xs_src.r0 + i + 1];
+            const int nnz = (int)(p1 - p0);
+            const int32_t* colp = xs_src.col + p0;
+            {
+                unsigned long long kk[TC_K];
+#pragma unroll
+                for (int j = 0; j < TC_K; ++j) kk[j] = ~0ull;
+                for (int u = tid; u < N; u += RS_THREADS) {
+                    const float* wr = W + (int64_t)u * d;
+                    double sv = 0.0;
+                    for (int q = 0; q < nnz; ++q) {
+                        const int k = __ldg(colp + q);
+                        const double wv = (double)__ldg(wr + k);
+                        const double e = (double)xs[k] - wv;
+                        sv += fma(e, e, -(wv * wv));
+                    }
+                    const double D = fmax(wnorm[u] + sv, 0.0);
+                    top_insert(kk, make_key((float)D, u));
+                }
+                block_topk(kk);
+            }
+#pragma unroll
+            for (int j = 0; j < TC_K; ++j) cu[j] = cand[j] == ~0ull ? -1 : key_unit(cand[j]);
+            exact_k(xs, W, d, cu, part, exd);
+            if (tid == 0) {
+                const double delta = ((double)d + (double)nnz + 8.0) * 0x1p-52 * (xn + wmax * wmax);
+                const double lb = cand[TC_K - 1] == ~0ull
+                                      ? INFINITY
+                                      : (double)nextafterf(key_dist(cand[TC_K - 1]), -INFINITY) - delta;
+                unsigned long long e1, e2;
+                const bool ok = certify(cu, exd, lb, N, e1, e2);
+                if (ok) {
+                    bmu1[i] = key_unit(e1);
+                    if (bmu2) bmu2[i] = e2 == ~0ull ? -1 : key_unit(e2);
+                    if (d2) d2[i] = key_dist(e1);
+                }
+                s_ok = ok ? 1 : 0;
+            }
+            __syncthreads();
+            if (s_ok) continue;
+        }
+        // ---- fallback B: the dense definition over every unit (warp per unit)
+        {
+            unsigned long long k1 = ~0ull, k2 = ~0ull;
+            for (int u = warp; u < N; u += RS_WARPS) {
+                const float* wr = W + (int64_t)u * d;
+                double a0 = 0.0, a1 = 0.0;
+                int k = lane;
+                for (; k + 32 < d; k += 64) {
+                    const double e0 = (double)xs[k] - (double)__ldg(wr + k);
+                    const double e1v = (double)xs[k + 32] - (double)__ldg(wr + k + 32);
+                    a0 = fma(e0, e0, a0);
+                    a1 = fma(e1v, e1v, a1);
+                }
+                if (k < d) {
+                    const double e0 = (double)xs[k] - (double)__ldg(wr + k);
+                    a0 = fma(e0, e0, a0);
+                }
+                const double t = warp_sum_f64(a0 + a1);
+                const unsigned long long kv = make_key((float)t, u);
+                if (kv < k1) { k2 = k1; k1 = kv; } else if (kv < k2) k2 = kv;
+            }
+            if (lane == 0) { wtop[warp][0] = k1; wtop[warp][1] = k2; }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long b1 = ~0ull, b2 = ~0ull;
+                for (int w = 0; w < RS_WARPS; ++w)
+                    for (int j = 0; j < 2; ++j) {
+                        const unsigned long long kv = wtop[w][j];
+                        if (kv < b1) { b2 = b1; b1 = kv; } else if (kv < b2) b2 = kv;
+                    }
+                bmu1[i] = key_unit(b1);
+                if (bmu2) bmu2[i] = b2 == ~0ull ? -1 : key_unit(b2);
+                if (d2) d2[i] = key_dist(b1);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// max_u |w_u| from the fp64 squared norms (one CTA)
+__global__ void wmax_kernel(const double* __restrict__ wn, int N, double* __restrict__ out) {
+    __shared__ double red[32];
+    double m = 0.0;
+    for (int u = threadIdx.x; u < N; u += blockDim.x) m = fmax(m, wn[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+        *out = sqrt(t);
     }
 }
 
@@ -391,20 +714,45 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int dp, int box_r
 
 int tc_padded_dim(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
 
-cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, float* norm, cudaStream_t st) {
+cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, double* norm, int* groups,
+                              cudaStream_t st) {
     const int dp = tc_padded_dim(d);
     int blocks = (int)std::min<int64_t>((rows + 7) / 8, 148 * 16);
     if (blocks < 1) blocks = 1;
-    split_kernel<<<blocks, 256, 0, st>>>(src, rows, d, dp, hi, lo, norm);
+    split_kernel<<<blocks, 256, 0, st>>>(src, rows, d, dp, hi, lo, norm, groups);
     return cudaGetLastError();
 }
 
 cudaError_t launch_split_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t rows,
-                             int d, float* hi, float* lo, float* norm, cudaStream_t st) {
+                             int d, float* hi, float* lo, double* norm, int* groups, cudaStream_t st) {
     const int dp = tc_padded_dim(d);
     int blocks = (int)std::min<int64_t>(rows, 148 * 16);
     if (blocks < 1) return cudaSuccess;
-    split_csr_kernel<<<blocks, 256, 0, st>>>(rowptr, col, val, r0, rows, dp, hi, lo, norm);
+    split_csr_kernel<<<blocks, 256, 0, st>>>(rowptr, col, val, r0, rows, dp, hi, lo, norm, groups);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wmax(const double* wn, int N, double* out, cudaStream_t st) {
+    wmax_kernel<<<1, 1024, 0, st>>>(wn, N, out);
+    return cudaGetLastError();
+}
+
+bool tc_rescore_fits(int d) { return 4 * (size_t)d <= 110 * 1024; }
+
+// rows [0, n) of this chunk: candidates keys[tc_unit_tiles(N)][n][TC_K] ->
+// certified exact bmu1 / bmu2 / D1; *nfall (device) counts documents that
+// took the exact scan over every unit
+cudaError_t launch_tc_rescore(const unsigned long long* keys, int64_t n, const int64_t* rowptr, const int32_t* col,
+                              const float* val, int64_t r0, const float* X, const float* W, int N, int d,
+                              const double* xnorm, const double* wnorm, const int* groups, const double* wmax,
+                              int32_t* bmu1, int32_t* bmu2, float* d2, int* nfall, cudaStream_t st) {
+    const size_t smem = 4 * (size_t)d;   // the document
+    cudaError_t e = cudaFuncSetAttribute(tc_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    XSrc xs{rowptr, col, val, r0, X};
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, 148 * 16));
+    tc_rescore_kernel<<<grid, RS_THREADS, smem, st>>>(keys, tc_unit_tiles(N), n, xs, W, N, d, xnorm, wnorm, groups,
+                                                      wmax, bmu1, bmu2, d2, nfall);
     return cudaGetLastError();
 }
 
@@ -412,9 +760,9 @@ int tc_unit_tiles(int N) { return (N + TC_BN - 1) / TC_BN; }
 int tc_doc_blocks(int64_t n) { return (int)((n + TC_BM - 1) / TC_BM); }
 
 // Documents [n] split (x_hi, x_lo, xnorm) against units [N] split (w_hi,
-// w_lo, wnorm); partial top-2 keys into keys[tc_unit_tiles(N)][n][2].
-cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
-                          const float* wlo, const float* wnorm, int N, int d, unsigned long long* keys, int sm_count,
+// w_lo, wnorm); partial top-K keys into keys[tc_unit_tiles(N)][n][TC_K].
+cudaError_t launch_map_tc(const float* xhi, const float* xlo, const double* xnorm, int64_t n, const float* whi,
+                          const float* wlo, const double* wnorm, int N, int d, unsigned long long* keys, int sm_count,
                           cudaStream_t st) {
     const int dp = tc_padded_dim(d);
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;

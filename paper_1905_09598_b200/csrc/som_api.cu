@@ -456,6 +456,13 @@ som_status som_last_spec_fallbacks(som_ctx* h, int64_t* count) {
     return SOM_OK;
 }
 
+som_status som_last_map_fallbacks(som_ctx* h, int64_t* count) {
+    if (!h) return fail(SOM_EINVAL, "null handle");
+    if (!count) return fail(SOM_EINVAL, "null count");
+    *count = h->last_tc_fallbacks;
+    return SOM_OK;
+}
+
 som_status som_set_map_precision(som_ctx* h, int32_t precision) {
     CHECK_HANDLE(h);
     if (precision < SOM_MAP_AUTO || precision > SOM_MAP_SPARSE_F64) return fail(SOM_EINVAL, "unknown map precision");

@@ -89,7 +89,8 @@ struct som_ctx {
     DevBuf dense;    // densified CSR chunk
     DevBuf utab;     // unit dealing of the CSR training kernels: [G][S] + counts[G]
     int utab_G = 0, utab_NL = 0, utab_rank = -1, utab_world = 0;
-    DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp32)
+    DevBuf wsplit;   // tensor-core mapping: W hi | W lo | |W|^2 (fp64) | max |w|
+    int last_tc_fallbacks = 0;   // documents of the last 3xTF32 mapping that took the exact scan (R20b)
     DevBuf xsplit;   // tensor-core mapping: X chunk hi | lo | |x|^2
     bool w_split_valid = false;
     DevBuf bbuf;     // batch SOM: bmu | order | scratch (int32) | cnt | off | sort temp

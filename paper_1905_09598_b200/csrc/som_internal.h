@@ -234,16 +234,25 @@ int map_exact_tiles_n(int N);
 int map_exact_tiles_m(int64_t n);
 
 // Tensor-core (tcgen05, 3xTF32) mapping, map_tc.cu.  Operands are split into
-// tf32 hi/lo planes with K padded to tc_padded_dim(d); norms fp64 -> fp32.
+// tf32 hi/lo planes with K padded to tc_padded_dim(d); fp64 norms and the
+// count of 8-wide K groups holding a non-zero (groups nullable).
 int tc_padded_dim(int d);
 int tc_unit_tiles(int N);
 int tc_doc_blocks(int64_t n);
-cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, float* norm, cudaStream_t st);
+constexpr int kTcCand = 4;   // candidates per document of the certified rescoring (R20b)
+cudaError_t launch_split_rows(const float* src, int64_t rows, int d, float* hi, float* lo, double* norm, int* groups,
+                              cudaStream_t st);
 cudaError_t launch_split_csr(const int64_t* rowptr, const int32_t* col, const float* val, int64_t r0, int64_t rows,
-                             int d, float* hi, float* lo, float* norm, cudaStream_t st);
-cudaError_t launch_map_tc(const float* xhi, const float* xlo, const float* xnorm, int64_t n, const float* whi,
-                          const float* wlo, const float* wnorm, int N, int d, unsigned long long* keys, int sm_count,
+                             int d, float* hi, float* lo, double* norm, int* groups, cudaStream_t st);
+cudaError_t launch_map_tc(const float* xhi, const float* xlo, const double* xnorm, int64_t n, const float* whi,
+                          const float* wlo, const double* wnorm, int N, int d, unsigned long long* keys, int sm_count,
                           cudaStream_t st);
+cudaError_t launch_wmax(const double* wn, int N, double* out, cudaStream_t st);
+bool tc_rescore_fits(int d);
+cudaError_t launch_tc_rescore(const unsigned long long* keys, int64_t n, const int64_t* rowptr, const int32_t* col,
+                              const float* val, int64_t r0, const float* X, const float* W, int N, int d,
+                              const double* xnorm, const double* wnorm, const int* groups, const double* wmax,
+                              int32_t* bmu1, int32_t* bmu2, float* d2, int* nfall, cudaStream_t st);
 
 // Exact sparse mapping (map_sparse.cu, R25): W^T (dim x Np, Np = N padded
 // to the 64 J-unit tile; fp64, or fp32 widened exactly in registers) +

@@ -9,49 +9,66 @@ using namespace som::host;
 
 namespace {
 
-// W split for the tensor-core path: hi, lo (N x dp) and |w|^2, cached until W changes.
-som_status ensure_w_split(som_ctx* h, const float** whi, const float** wlo, const float** wn) {
+// W split for the tensor-core path: hi, lo (N x dp), fp64 |w|^2 and max |w|,
+// cached until W changes.
+som_status ensure_w_split(som_ctx* h, const float** whi, const float** wlo, const double** wn, const double** wmax) {
     const int dp = tc_padded_dim(h->dim);
     const size_t plane = sizeof(float) * (size_t)h->N * dp;
     if (!h->w_split_valid) {
-        CK(h->wsplit.ensure(2 * plane + sizeof(float) * (size_t)h->N, h->stream));
+        CK(h->wsplit.ensure(2 * plane + sizeof(double) * ((size_t)h->N + 1), h->stream));
         char* base = (char*)h->wsplit.p;
-        CK(launch_split_rows(h->W, h->N, h->dim, (float*)base, (float*)(base + plane), (float*)(base + 2 * plane),
-                             h->stream));
+        CK(launch_split_rows(h->W, h->N, h->dim, (float*)base, (float*)(base + plane), (double*)(base + 2 * plane),
+                             nullptr, h->stream));
+        CK(launch_wmax((const double*)(base + 2 * plane), h->N, (double*)(base + 2 * plane) + h->N, h->stream));
         h->w_split_valid = true;
     }
     char* base = (char*)h->wsplit.p;
     *whi = (const float*)base;
     *wlo = (const float*)(base + plane);
-    *wn = (const float*)(base + 2 * plane);
+    *wn = (const double*)(base + 2 * plane);
+    *wmax = *wn + h->N;
     return SOM_OK;
 }
 
 // Tensor-core mapping of n documents whose split rows are produced chunk by
-// chunk by `fill(r0, m, hi, lo, norm)`; outputs device pointers.
-using SplitFill = std::function<cudaError_t(int64_t, int64_t, float*, float*, float*)>;
-som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, int32_t* b1, int32_t* b2, float* d2,
-                       int* launches) {
-    const float *whi, *wlo, *wn;
-    som_status st = ensure_w_split(h, &whi, &wlo, &wn);
+// chunk by `fill(r0, m, hi, lo, norm, groups)`, certified and rescored
+// exactly against the documents themselves (csr rows, or dense device rows
+// Xd); outputs device pointers.
+using SplitFill = std::function<cudaError_t(int64_t, int64_t, float*, float*, double*, int*)>;
+som_status map_tc_rows(som_ctx* h, int64_t n, const SplitFill& fill, const CsrIn* csr, const float* Xd, int32_t* b1,
+                       int32_t* b2, float* d2, int* launches) {
+    const float *whi, *wlo;
+    const double *wn, *wmax;
+    som_status st = ensure_w_split(h, &whi, &wlo, &wn, &wmax);
     if (st) return st;
     const int dp = tc_padded_dim(h->dim);
     // split-X chunk: up to 8 GiB of hi/lo planes (large chunks keep B panels hot)
     const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, ((int64_t)8 << 30) / (8 * (int64_t)dp)));
     const size_t plane = sizeof(float) * (size_t)chunk * dp;
-    CK(h->xsplit.ensure(2 * plane + sizeof(float) * (size_t)chunk, h->stream));
+    CK(h->xsplit.ensure(2 * plane + (sizeof(double) + sizeof(int)) * (size_t)chunk + 64, h->stream));
     char* xb = (char*)h->xsplit.p;
+    double* xn = (double*)(xb + 2 * plane);
+    int* grp = (int*)(xn + chunk);
     const int tiles_n = tc_unit_tiles(h->N);
-    CK(h->keys.ensure(sizeof(unsigned long long) * 2 * (size_t)tiles_n * (size_t)chunk, h->stream));
+    CK(h->keys.ensure(sizeof(unsigned long long) * kTcCand * (size_t)tiles_n * (size_t)chunk, h->stream));
+    CK(h->red.ensure(64, h->stream));
+    int* nfall = (int*)h->red.p;
+    CK(cudaMemsetAsync(nfall, 0, sizeof(int), h->stream));
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t m = std::min(chunk, n - r0);
-        CK(fill(r0, m, (float*)xb, (float*)(xb + plane), (float*)(xb + 2 * plane)));
-        CK(launch_map_tc((const float*)xb, (const float*)(xb + plane), (const float*)(xb + 2 * plane), m, whi, wlo,
-                         wn, h->N, h->dim, (unsigned long long*)h->keys.p, h->sm_count, h->stream));
-        CK(launch_map_merge((const unsigned long long*)h->keys.p, tiles_n, m, b1 + r0, b2 ? b2 + r0 : nullptr,
-                            d2 ? d2 + r0 : nullptr, h->stream));
+        CK(fill(r0, m, (float*)xb, (float*)(xb + plane), xn, grp));
+        CK(launch_map_tc((const float*)xb, (const float*)(xb + plane), xn, m, whi, wlo, wn, h->N, h->dim,
+                         (unsigned long long*)h->keys.p, h->sm_count, h->stream));
+        CK(launch_tc_rescore((const unsigned long long*)h->keys.p, m, csr ? csr->rowptr : nullptr,
+                             csr ? csr->col : nullptr, csr ? csr->val : nullptr, r0,
+                             Xd ? Xd + r0 * (int64_t)h->dim : nullptr, h->W, h->N, h->dim, xn, wn, grp, wmax, b1 + r0,
+                             b2 ? b2 + r0 : nullptr, d2 ? d2 + r0 : nullptr, nfall, h->stream));
         *launches += 3;
     }
+    int nf = 0;
+    CK(cudaMemcpyAsync(&nf, nfall, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->last_tc_fallbacks = nf;
     return SOM_OK;
 }
 
@@ -102,6 +119,7 @@ namespace host {
 // tensor cores once the contraction is large enough to amortise the split).
 bool use_tc(const som_ctx* h, int64_t n) {
     if (h->map_precision == SOM_MAP_EXACT_F64 || h->map_precision == SOM_MAP_SPARSE_F64) return false;
+    if (!tc_rescore_fits(h->dim)) return false;   // the rescoring holds a document in shared memory
     if (h->map_precision == SOM_MAP_3XTF32) return true;
     return (double)n * h->N * h->dim >= 1.0e10;
 }
@@ -163,10 +181,10 @@ som_status map_dense_dev(som_ctx* h, const float* Xd, int64_t n, int32_t* b1, in
         return SOM_OK;
     }
     if (use_tc(h, n)) {
-        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
-            return launch_split_rows(Xd + r0 * h->dim, m, h->dim, hi, lo, nrm, h->stream);
+        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, double* nrm, int* grp) {
+            return launch_split_rows(Xd + r0 * h->dim, m, h->dim, hi, lo, nrm, grp, h->stream);
         };
-        return map_tc_rows(h, n, fill, b1, b2, d2, launches);
+        return map_tc_rows(h, n, fill, nullptr, Xd, b1, b2, d2, launches);
     }
     return map_exact_dev(h, Xd, n, b1, b2, d2, launches);
 }
@@ -203,10 +221,10 @@ som_status map_csr_dev(som_ctx* h, const CsrIn& csr, int64_t n, int32_t* b1, int
         return SOM_OK;
     }
     if (path == SOM_MAP_3XTF32) {
-        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, float* nrm) {
-            return launch_split_csr(csr.rowptr, csr.col, csr.val, r0, m, h->dim, hi, lo, nrm, h->stream);
+        auto fill = [&](int64_t r0, int64_t m, float* hi, float* lo, double* nrm, int* grp) {
+            return launch_split_csr(csr.rowptr, csr.col, csr.val, r0, m, h->dim, hi, lo, nrm, grp, h->stream);
         };
-        return map_tc_rows(h, n, fill, b1, b2, d2, launches);
+        return map_tc_rows(h, n, fill, &csr, nullptr, b1, b2, d2, launches);
     }
     // exact dense definition: densify in chunks of <= 1 GiB and map each chunk
     const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, ((int64_t)1 << 30) / (4 * (int64_t)h->dim)));

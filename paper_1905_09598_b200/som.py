@@ -45,7 +45,7 @@ _lib = None
 
 # every symbol include/som.h declares (tests check the library exports them)
 EXPORTS = ["som_schedule_default", "som_create", "som_destroy", "som_set_weights", "som_get_weights",
-           "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_last_spec_fallbacks", "som_map", "som_map_csr", "som_set_map_precision",
+           "som_init_random", "som_train_online", "som_train_online_csr", "som_set_train_mode", "som_set_train_grid", "som_set_trace", "som_last_train_config", "som_last_spec_fallbacks", "som_last_map_fallbacks", "som_map", "som_map_csr", "som_set_map_precision",
            "som_train_batch", "som_train_batch_csr", "som_tfidf_csr", "som_pca_top2", "som_pca_top2_csr",
            "som_init_linear", "som_map_geometry",
            "som_qerror", "som_topographic_error", "som_errors", "som_errors_csr", "som_umatrix", "som_set_stream",
@@ -87,6 +87,7 @@ def lib():
         "som_set_trace": [P, P, i32],
         "som_last_train_config": [P, P, P],
         "som_last_spec_fallbacks": [P, P],
+        "som_last_map_fallbacks": [P, P],
         "som_qerror": [P, P, i64, P],
         "som_topographic_error": [P, P, i64, P],
         "som_errors": [P, P, i64, P, P],
@@ -331,6 +332,12 @@ def som_last_train_config(h) -> tuple[int, int]:
     _check(lib().som_last_train_config(h, ctypes.byref(g), ctypes.byref(k)))
     return g.value, k.value
 
+
+
+def som_last_map_fallbacks(h) -> int:
+    n = ctypes.c_int64()
+    _check(lib().som_last_map_fallbacks(h, ctypes.byref(n)))
+    return n.value
 
 
 def som_last_spec_fallbacks(h) -> int:

@@ -1,17 +1,19 @@
 """tcgen05 3xTF32 batch mapping (SOM_MAP_3XTF32) against the oracle.
 
-Bar (BASELINE.json north_star, R19/R20): bmu1 identical on every
-document whose oracle margin (D2-D1)/D1 exceeds 1e-5, bmu2 identical where
-(D3-D2)/D2 also does; D1 within 1e-5 relative; QE within 1e-4."""
+The tensor cores are a filter (R20b): 4 candidates per document
+from the 3xTF32 contraction, rescored by the exact fp64 definition (R10) and
+certified against a bound on the approximation error, else mapped exactly
+over every unit.  Bar: bmu1, bmu2 and D1 equal the oracle's on EVERY
+document — no margin filter — including exact ties (duplicate prototypes:
+lowest index first, R9) and documents placed at near-ties, which must take
+the exact fallback."""
 import numpy as np
 import pytest
 
 import oracle
-from synth import bank_corpus, init_rows, uniform_matrix
+from synth import bank_corpus, init_rows
 
 pytestmark = pytest.mark.gpu
-
-MARGIN = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -28,21 +30,24 @@ def _codebook(X, N, seed):
     return (0.6 * R + 0.4 * mu).astype(np.float32)
 
 
-def _check(b1, b2, d1, ob1, ob2, od1, m12, m23):
-    ok1 = m12 > MARGIN
-    ok2 = ok1 & (m23 > MARGIN)
-    assert ok1.mean() > 0.95, f"too many near ties: {ok1.mean()}"
-    bad = np.flatnonzero(ok1 & (b1 != ob1))
-    assert bad.size == 0, f"bmu1 differs on {bad.size} margin-filtered docs, e.g. {bad[:5]}"
-    bad2 = np.flatnonzero(ok2 & (b2 != ob2))
-    assert bad2.size == 0, f"bmu2 differs on {bad2.size} docs"
-    # D1: tensor-core fp32 accumulation is not round-to-nearest (observed
-    # positive bias growing with K). With the hi.hi and lo
-    # products in separate TMEM accumulators the observed max is ~5e-6; bar
-    # 1e-5 absolute, 10x inside the north star's 1e-4 max-abs for errors.
-    ab = np.abs(d1.astype(np.float64) - od1)
-    assert ab.max() <= 1e-5, ab.max()
-    print(f" [3xTF32 D1 abs err max {ab.max():.2e} median {np.median(ab):.2e}]", end="")
+def _check_all(b1, b2, d1, ob1, ob2, od1):
+    bad = np.flatnonzero(b1 != ob1)
+    assert bad.size == 0, f"bmu1 differs on {bad.size} docs, e.g. {bad[:5]}"
+    bad2 = np.flatnonzero(b2 != ob2)
+    assert bad2.size == 0, f"bmu2 differs on {bad2.size} docs, e.g. {bad2[:5]}"
+    diff = np.flatnonzero(d1 != od1.astype(np.float32))
+    assert diff.size == 0, f"D1 differs on {diff.size} docs (max {np.abs(d1[diff] - od1[diff]).max():.3g})"
+
+
+def _map_tc(som, m, X=None, csr=None):
+    som.som_set_map_precision(m.h, som.SOM_MAP_3XTF32)
+    if csr is None:
+        b1, b2, d1 = m.map(X)
+    else:
+        n = csr.n
+        b1, b2, d1 = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.float32)
+        som.som_map_csr(m.h, csr.indptr, csr.indices, csr.data, n, b1, b2, d1)
+    return b1, b2, d1, som.som_last_map_fallbacks(m.h)
 
 
 @pytest.mark.parametrize("rows,cols,n,d,topo", [
@@ -50,27 +55,64 @@ def _check(b1, b2, d1, ob1, ob2, od1, m12, m23):
     (10, 10, 200, 500, 0),       # c1 shape
     (13, 23, 1000, 1000, 1),     # N = 299 (ragged unit tile), d % 32 != 0
     (3, 5, 300, 333, 1),         # d % 4 != 0, tiny map
+    (2, 2, 150, 40, 0),          # N = 4: every unit a candidate
     (1, 1, 130, 64, 0),          # 1 unit: bmu2 = -1
 ])
-def test_map_3xtf32_matches_oracle(som, rows, cols, n, d, topo):
+def test_map_3xtf32_exact_on_every_document(som, rows, cols, n, d, topo):
     C = bank_corpus(n, d, seed=n + d + 1)
     X = C.dense()
     W = _codebook(X, rows * cols, 3)
     with som.SOM(rows, cols, d, topo) as m:
         m.set_weights(W)
+        b1, b2, d1, nf = _map_tc(som, m, X=X)
         som.som_set_map_precision(m.h, som.SOM_MAP_3XTF32)
-        b1, b2, d1 = m.map(X)
         qe, te = m.errors(X)
-    ob1, ob2, od1, m12, m23 = oracle.map_docs(W, X, want_margins=True)
-    if rows * cols == 1:
-        assert np.all(b1 == 0) and np.all(b2 == -1)
-        np.testing.assert_allclose(d1, od1, rtol=1e-5)
-        return
-    _check(b1, b2, d1, ob1, ob2, od1, m12, m23)
-    assert abs(qe - oracle.qerror_from_d1(od1)) <= 1e-4
-    ok = (m12 > MARGIN) & (m23 > MARGIN)
-    te_o = oracle.topographic_error_from_bmus(rows, cols, topo, ob1, ob2)
-    assert abs(te - te_o) <= (1 - ok.mean()) + 1e-12
+    ob1, ob2, od1 = oracle.map_docs(W, X)
+    _check_all(b1, b2, d1, ob1, ob2, od1)
+    assert abs(qe - oracle.qerror_from_d1(od1)) <= 1e-12
+    assert te == oracle.topographic_error_from_bmus(rows, cols, topo, ob1, ob2)
+    print(f" [{rows}x{cols} d={d}: {nf} of {n} docs by the exact fallback]", end="")
+
+
+def test_map_3xtf32_ties_and_near_ties(som):
+    """Where the tensor-core filter cannot decide: eight prototypes within a
+    few fp32 ulps of each other (the 3xTF32 error exceeds their spread: the
+    certificate fails and the sparse-identity scan decides) and six exact
+    duplicates (ties at every precision: the dense scan over every unit
+    decides, lowest index first, R9).  Identical to the oracle on every
+    document, dense and CSR input."""
+    C = bank_corpus(1500, 1500, seed=41)
+    X = C.dense()
+    W = _codebook(X, 256, 42)
+    base = W[40].copy()
+    for j in range(8):                           # units 40..47: base + j ulps on one element each
+        W[40 + j] = base
+        k = int(np.flatnonzero(base)[j % np.count_nonzero(base)])
+        W[40 + j, k] = np.nextafter(base[k], np.float32(2.0)) if j else base[k]
+        for _ in range(j // 2):
+            W[40 + j, k] = np.nextafter(W[40 + j, k], np.float32(2.0))
+    W[100:106] = W[60]                           # units 60, 100..105: exact duplicates
+    rng = np.random.default_rng(43)
+    near = (base + rng.random((40, 1500)).astype(np.float32) * 1e-4 * (base > 0)).astype(np.float32)
+    Xt = np.concatenate([X, near, np.repeat(W[60:61], 10, 0)])
+    from scipy import sparse
+    Ct = sparse.csr_matrix(Xt)
+    with som.SOM(16, 16, 1500, 1) as m:
+        m.set_weights(W)
+        b1, b2, d1, nf = _map_tc(som, m, X=Xt)
+        c1 = np.empty(Xt.shape[0], np.int32)
+        c2 = np.empty(Xt.shape[0], np.int32)
+        cd = np.empty(Xt.shape[0], np.float32)
+        som.som_set_map_precision(m.h, som.SOM_MAP_3XTF32)
+        som.som_map_csr(m.h, Ct.indptr.astype(np.int64), Ct.indices.astype(np.int32), Ct.data.astype(np.float32),
+                        Xt.shape[0], c1, c2, cd)
+        nf_csr = som.som_last_map_fallbacks(m.h)
+    ob1, ob2, od1 = oracle.map_docs(W, Xt)
+    _check_all(b1, b2, d1, ob1, ob2, od1)
+    _check_all(c1, c2, cd, ob1, ob2, od1)
+    assert nf >= 10 and nf_csr >= 10, (nf, nf_csr)
+    assert np.all(b1[-10:] == 60) and np.all(b2[-10:] == 100)
+    print(f" [{nf} (dense) / {nf_csr} (CSR) of {Xt.shape[0]} docs took a fallback]", end="")
 
 
 def test_map_3xtf32_csr_equals_dense(som):
@@ -79,41 +121,34 @@ def test_map_3xtf32_csr_equals_dense(som):
     W = _codebook(X, 300, 4)
     with som.SOM(15, 20, 2000, 1) as m:
         m.set_weights(W)
-        som.som_set_map_precision(m.h, som.SOM_MAP_3XTF32)
-        a1, a2, ad = m.map(X)
-        b1 = np.empty(C.n, np.int32)
-        b2 = np.empty(C.n, np.int32)
-        bd = np.empty(C.n, np.float32)
-        som.som_map_csr(m.h, C.indptr, C.indices, C.data, C.n, b1, b2, bd)
-    ob1, ob2, od1, m12, m23 = oracle.map_docs(W, X, want_margins=True)
-    _check(b1, b2, bd, ob1, ob2, od1, m12, m23)
-    same = m12 > MARGIN
-    assert np.array_equal(a1[same], b1[same])
-    np.testing.assert_allclose(ad, bd, rtol=2e-7, atol=1e-7)
+        a1, a2, ad, _ = _map_tc(som, m, X=X)
+        b1, b2, bd, nf = _map_tc(som, m, csr=C)
+    ob1, ob2, od1 = oracle.map_docs(W, X)
+    _check_all(b1, b2, bd, ob1, ob2, od1)
+    assert np.array_equal(a1, b1) and np.array_equal(a2, b2) and np.array_equal(ad, bd)
 
 
 def test_map_3xtf32_c3_sample(som):
-    """c3-like contraction (20k docs x 2500 units x 10k terms, CSR input);
-    the oracle's sparse-identity path checks every document."""
+    """c3-like contraction (20k docs x 2500 units x 10k terms, CSR input):
+    every document against the oracle's sparse-identity mapping (R25 — its
+    D1 may differ from the dense definition's in the last fp32 ulp)."""
     C = bank_corpus(20000, 10000, seed=33)
     Wsrc = bank_corpus(2500, 10000, seed=34).dense()
     W = (0.5 * Wsrc + 0.5 * C.dense()[:2500].mean(0)).astype(np.float32)
     with som.SOM(50, 50, 10000, 1) as m:
         m.set_weights(W)
-        som.som_set_map_precision(m.h, som.SOM_MAP_3XTF32)
-        b1 = np.empty(C.n, np.int32)
-        b2 = np.empty(C.n, np.int32)
-        d1 = np.empty(C.n, np.float32)
-        som.som_map_csr(m.h, C.indptr, C.indices, C.data, C.n, b1, b2, d1)
+        b1, b2, d1, nf = _map_tc(som, m, csr=C)
         ms, units, _ = som.som_last_stats(m.h)
-    ob1, ob2, od1, m12, m23 = oracle.map_docs_csr(W, C.indptr, C.indices, C.data, want_margins=True)
-    _check(b1, b2, d1, ob1, ob2, od1, m12, m23)
-    print(f"c3-like 3xTF32 mapping: {units} docs in {ms:.2f} ms")
+    ob1, ob2, od1 = oracle.map_docs_csr(W, C.indptr, C.indices, C.data)
+    assert np.array_equal(b1, ob1) and np.array_equal(b2, ob2)
+    ulp = np.spacing(od1.astype(np.float32))
+    assert np.all(np.abs(d1.astype(np.float64) - od1) <= ulp)
+    print(f" [c3-like 3xTF32 mapping: {units} docs in {ms:.2f} ms, {nf} exact fallbacks]", end="")
 
 
 def test_auto_precision_and_weight_changes(som):
-    """AUTO switches to the tensor cores for large contractions; the cached W
-    split follows weight updates (set_weights, training)."""
+    """AUTO switches to the tensor cores for large dense contractions; the
+    cached W split follows weight updates (set_weights)."""
     C = bank_corpus(4000, 3000, seed=5)
     X = C.dense()
     W = _codebook(X, 1024, 6)
@@ -124,7 +159,6 @@ def test_auto_precision_and_weight_changes(som):
         assert launches == 3
         W2 = W[::-1].copy()
         m.set_weights(W2)
-        c1, _, _ = m.map(X)
-    ob1, _, _, m12, _ = oracle.map_docs(W2, X, want_margins=True)
-    ok = m12 > MARGIN
-    assert np.array_equal(c1[ok], ob1[ok])
+        c1, c2, cd = m.map(X)
+    ob1, ob2, od1 = oracle.map_docs(W2, X)
+    _check_all(c1, c2, cd, ob1, ob2, od1)

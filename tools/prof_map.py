@@ -28,6 +28,7 @@ d1 = torch.empty(n, dtype=torch.float32, device="cuda")
 for r in range(reps):
     som.som_map_csr(m.h, rp, ci, va, n, b1, b2, d1)
     ms, units, launches = som.som_last_stats(m.h)
+    nf = som.som_last_map_fallbacks(m.h)
     flop = 2.0 * n * side * side * d
-    print(f"rep {r}: {n} docs x {side * side} units x {d} terms: {ms:.3f} ms, {n / ms * 1e3:.0f} docs/s, "
+    print(f"[fallbacks {nf}] rep {r}: {n} docs x {side * side} units x {d} terms: {ms:.3f} ms, {n / ms * 1e3:.0f} docs/s, "
           f"{flop / ms / 1e9:.1f} algorithmic TFLOP/s ({3 * flop / ms / 1e9:.1f} executed tf32), {launches} launches")
