@@ -16,7 +16,9 @@
 //                      own path beside the shared-memory port); updated rows
 //                      are also written through to W (the sparse sums below
 //                      gather from W, and only the owning warp can read a
-//                      TMEM lane);
+//                      TMEM lane) — while every unit is updated every step
+//                      only at x_t's non-zeros, fully once the speculative
+//                      sums run (after one catch-up of every TMEM row);
 //   [ntm, non)         shared memory, [row][j][dt] float4 (conflict-free);
 //   [non, S)           W in global memory (L2-resident: only these rows are
 //                      read during the launch), streamed through a ring of
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
     const uint32_t tm_base_off = ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((dw >> 2) * kTmCols);
 
     uint32_t mp = 0u, mc = 0u;   // non-zeros of x_{t-1}, x_t among this thread's elements
+    bool tm_stale = false;       // some TMEM row's copy in W is partial (full-coverage steps)
     float4 xp[KJ];               // x_{t-1} at this thread's elements (the pending update's sample)
     auto tm_addr = [&](int r) { return s_tmem + tm_base_off + (uint32_t)(r * 4 * KJ); };
     auto bounds = [&](int64_t t) {
@@ -472,7 +475,19 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
 #pragma unroll
                     for (int j = 0; j < KJ; ++j) {
                         w[j] = eq1u(h, w[j], xp[j]);
-                        if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, w[j]);   // write-through
+                        if (spec) {
+                            if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, w[j]);   // write-through
+                        } else {
+                            // only x_t's non-zeros: the gathers below read nothing else
+                            const uint32_t bits = (mc >> (4 * j)) & 0xFu;
+                            if (bits) {
+                                float* g = reinterpret_cast<float*>(grow + j * NDT);
+                                if (bits & 1u) __stcg(g, w[j].x);
+                                if (bits & 2u) __stcg(g + 1, w[j].y);
+                                if (bits & 4u) __stcg(g + 2, w[j].z);
+                                if (bits & 8u) __stcg(g + 3, w[j].w);
+                            }
+                        }
                         const double e0 = w[j].x, e1 = w[j].y, e2 = w[j].z, e3 = w[j].w;
                         n0 = fma(e0, e0, n0); n1 = fma(e1, e1, n1); n0 = fma(e2, e2, n0); n1 = fma(e3, e3, n1);
                     }
@@ -504,6 +519,21 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
                 push(s, n0 + n1);
             }
             push_flush();
+            if (!spec && nord > 0 && ntm > 0) tm_stale = true;
+            if (spec && tm_stale) {
+                // TMEM rows were written through partially (full-coverage
+                // steps): W catches up once before the speculative gathers
+                twait_st();
+                for (int s2 = 0; s2 < ntm && s2 < Sb; ++s2) {
+                    float4 w[KJ];
+                    tm_load<KJ>(tm_addr(s2), w);
+                    float4* grow = W4 + (int64_t)uid[s2] * d4 + dt;
+#pragma unroll
+                    for (int j = 0; j < KJ; ++j)
+                        if (j < KJ - 1 || vlast) __stcg(grow + j * NDT, w[j]);
+                }
+                tm_stale = false;
+            }
             twait_st();
             if (tr1) tr1[1] = trace_now(a.trace_clk);
             if (nord > 0) {
