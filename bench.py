@@ -825,7 +825,7 @@ def run_b200(args, rank, world, local):
         if os.path.exists(tp):
             with open(tp) as f:
                 tj = json.load(f)
-            traffic = tj.get("bytes_per_launch")
+            traffic = tj.get("bytes_per_launch") if tj.get("kernel_id", k_used) == k_used else None
         kname = {3: "som_train_tma_kernel (dense rows, W streamed)", 4: "som_train_csr_tma_kernel (sparse distances, "
                  "W streamed through L2)", 2: "som_train_reg_kernel (W in registers)",
                  10: "som_train_tier_kernel (W in TMEM + smem + a streamed remainder, sparse distances)",
