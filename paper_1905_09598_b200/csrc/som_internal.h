@@ -65,6 +65,10 @@ struct TrainArgs {
     const int* ucnt;
     // train_spec.cu: count of steps that took the exact fallback (nullable)
     unsigned long long* spec_fallbacks;
+    // in-GPU exchange (xchg_publish / xchg_wait below): 0 = tagged
+    // all-gather, 1 = one atomic max + an arrival counter, 2 = the tagged
+    // all-gather read once a relaxed arrival counter says it is complete
+    int xchg_atomic;
 };
 
 constexpr int kTracePhases = 8;
@@ -102,7 +106,36 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned 
 // returns with *stop = 1 (the host reports SOM_ECUDA, never hangs).
 __device__ __forceinline__ unsigned long long xchg_tag(int64_t t) { return 0x80ull | (unsigned long long)(t & 0x7F); }
 
+// Atomic variant (a.xchg_atomic): words [2 xstride, 2 xstride + 64) of the
+// exchange buffer (zeroed before every launch) hold an arrival counter C
+// (line 0) and three step words M[k] (lines 1..3).  Step t uses
+// M[(t - t0) % 3]: every CTA does red.max(M, ~key) then
+// red.add.release(C, 1); the wait polls C with acquire loads until it
+// reaches G (t - t0 + 1), then reads M (its max of complemented keys is the
+// min key: lowest (D, u), R9).  CTA 0 clears M[(t - 1 - t0) % 3] after the
+// wait of step t: every CTA read it before arriving at step t, and nobody
+// writes it again before step t + 2, whose writes follow CTA 0's arrival at
+// step t + 1 (release) in every CTA's acquire order.
+__device__ __forceinline__ unsigned long long* xa_count(const TrainArgs& a) { return a.xchg + 2 * (size_t)a.xstride; }
+__device__ __forceinline__ unsigned long long* xa_word(const TrainArgs& a, int64_t t) {
+    return a.xchg + 2 * (size_t)a.xstride + 16 * (1 + (int)((t - a.t0) % 3));
+}
+
 __device__ __forceinline__ void xchg_publish(const TrainArgs& a, unsigned long long key, int64_t t, int b, int lane) {
+    if (a.xchg_atomic == 2) {   // tagged slot + relaxed arrival count (a polling hint)
+        if (lane == 0) {
+            st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.xstride + b, (key & ~0xFFull) | xchg_tag(t));
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(xa_count(a)) : "memory");
+        }
+        return;
+    }
+    if (a.xchg_atomic) {
+        if (lane == 0) {
+            asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(xa_word(a, t)), "l"(~(key | 0xFFull)) : "memory");
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(xa_count(a)) : "memory");
+        }
+        return;
+    }
     if (lane == 0) st_relaxed_u64(a.xchg + (size_t)(t & 1) * a.xstride + b, (key & ~0xFFull) | xchg_tag(t));
 }
 
@@ -123,7 +156,27 @@ __device__ __forceinline__ unsigned long long xchg_wait(const TrainArgs& a, int6
     const unsigned long long* slots = a.xchg + (size_t)(t & 1) * a.xstride;
     unsigned long long gmin = 0;
     Spin spins;
-    for (;;) {
+    if (a.xchg_atomic == 2) {   // wait for the count, then read (and validate) the tagged slots
+        const unsigned long long want = (unsigned long long)a.G * (unsigned long long)(t - a.t0 + 1);
+        for (;;) {
+            const unsigned long long c = __shfl_sync(0xffffffffu, ld_relaxed_u64(xa_count(a)), 0);
+            if (c >= want) break;
+            if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
+            if (a.poll_ns > 0) __nanosleep(a.poll_ns);
+        }
+    } else if (a.xchg_atomic) {
+        const unsigned long long want = (unsigned long long)a.G * (unsigned long long)(t - a.t0 + 1);
+        for (;;) {
+            unsigned long long c;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(xa_count(a)) : "memory");
+            if (__shfl_sync(0xffffffffu, c, 0) >= want) break;
+            if (xchg_should_stop(a, spins, lane)) { *stop = 1; return 0; }
+            if (a.poll_ns > 0) __nanosleep(a.poll_ns);
+        }
+        gmin = (~ld_relaxed_u64(xa_word(a, t)) & ~0xFFull) | tag;
+        if (b == 0 && lane == 0 && t > a.t0) st_relaxed_u64(xa_word(a, t - 1), 0ull);
+    }
+    for (; a.xchg_atomic != 1;) {
         unsigned long long m = ~0ull;
         bool ok = true;
         for (int j = lane; j < a.G; j += 32) {

@@ -290,6 +290,15 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     // lines (a line shared by step t's and step t+1's slots would be written
     // by fast CTAs while slow ones still poll it)
     a.xstride = (a.G + 31) & ~31;
+    // exchange variant (som_internal.h), measured on B200 (tools/xchg_ab.py,
+    // bit-identical results): the tagged all-gather alone is fastest for
+    // small grids (c1, G = 32: 2.27 vs 2.46 us/step); from ~100 CTAs on, the
+    // all-gather read once a relaxed arrival counter is complete wins (c2,
+    // G = 128: 3.24 vs 3.27; c3, G = 148: 23.0 vs 24.0 us/step early in the
+    // schedule, 5.9 vs 7.5 late), the L2 no longer serving G full scans per
+    // poll round
+    a.xchg_atomic = a.G >= 96 ? 2 : 0;
+    if (const char* e = std::getenv("SOM_XCHG_ATOMIC")) a.xchg_atomic = std::max(0, std::min(2, std::atoi(e)));
     a.poll_ns = 0;
     if (const char* e = std::getenv("SOM_POLL_NS")) a.poll_ns = std::max(0, std::atoi(e));
     // exchange wait bound: 60 s of %globaltimer (SOM_SPIN_TIMEOUT_MS), then

@@ -1,0 +1,2 @@
+timeout 1200 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
