@@ -323,26 +323,53 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
     const char* spec_env = std::getenv("SOM_TRAIN_SPEC");
     const int spec_mode = spec_env ? std::atoi(spec_env) : 0;
     if (use_reg && spec_mode == 1 && train_spec_supported(a.S, h->dim, a.G, h->world)) use_spec = true;
-    // kernel 10 while the neighbourhood covers the whole lattice (every unit
-    // updated every step: its on-chip rows save the most), then kernel 4
+    // kernel 10 while the neighbourhood covers most of the lattice (its
+    // on-chip rows save the most when most units are updated), then kernel 4
     // (few updated units: kernel 4's step is shorter); an exact t-range
-    // split, both kernels give identical results.  SOM_TIER_HANDOVER=0:
-    // kernel 10 throughout.
+    // split, both kernels give identical results.  The hand-over is the
+    // first step whose cutoff disk holds, on average over winner positions
+    // (64 sampled units), less than SOM_TIER_COVER (default 0.4) of the
+    // units: c3 per 20,000-step segment (tools/prof_tier.py, B200) kernel 10
+    // is faster down to ~0.4 mean coverage (t ~ 300k: 15.0 vs 15.1 us/step),
+    // kernel 4 after (13.1 vs 12.9).  SOM_TIER_HANDOVER=0: kernel 10 throughout.
     int64_t t_tier = t_end;
     if (use_tier && a.cutoff_on) {
         bool handover = true;
         if (const char* e = std::getenv("SOM_TIER_HANDOVER")) handover = std::atoi(e) != 0;
+        double thr = 0.4;
+        if (const char* e = std::getenv("SOM_TIER_COVER")) thr = std::atof(e);
         if (handover) {
-            auto full_cover = [&](int64_t t) {
+            const int Nm = h->rows * h->cols;
+            const int stride = std::max(1, Nm / 64);
+            auto mean_cover = [&](int64_t t) {
                 double f;
                 fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
                 const double sigma = std::max(sd.sigma_min, sigma0 * f);
-                return 2.0 * sigma * sigma * a.ln_inv_eps >= a.g2max;
+                const double r2 = 2.0 * sigma * sigma * a.ln_inv_eps;
+                int64_t cnt = 0, pos = 0;
+                for (int c = stride / 2; c < Nm; c += stride, ++pos) {
+                    const int ic = c / h->cols, jc = c - ic * h->cols;
+                    for (int i = 0; i < h->rows; ++i) {
+                        const double di = (double)(i - ic);
+                        for (int j = 0; j < h->cols; ++j) {
+                            double g2;
+                            if (h->topo == 0) {
+                                const double dj = (double)(j - jc);
+                                g2 = di * di + dj * dj;
+                            } else {
+                                const double dx2 = (double)(2 * (j - jc) + ((i & 1) - (ic & 1)));
+                                g2 = 0.25 * dx2 * dx2 + 0.75 * di * di;
+                            }
+                            cnt += g2 <= r2;
+                        }
+                    }
+                }
+                return (double)cnt / ((double)pos * Nm);
             };
-            int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) not fully covered
+            int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) below the threshold (non-increasing in t)
             while (lo < hi) {
                 const int64_t mid = lo + (hi - lo) / 2;
-                if (full_cover(mid)) lo = mid + 1; else hi = mid;
+                if (mean_cover(mid) >= thr) lo = mid + 1; else hi = mid;
             }
             t_tier = lo;
         }

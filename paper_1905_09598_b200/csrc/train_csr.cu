@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         xd[j][0] = xc[j].x; xd[j][1] = xc[j].y; xd[j][2] = xc[j].z; xd[j][3] = xc[j].w;
     }
     int64_t q = 0;   // rows consumed from the ring so far (CTA-uniform)
+    double f_next = a.t1 > a.t0 ? a.f_tab[0] : 0.0;   // decay factor of the coming step, loaded a step ahead
 
     for (int64_t t = a.t0; t < a.t1; ++t) {
         unsigned long long* tr = nullptr;   // optional phase trace (som_set_trace)
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         q += nup;   // the last row's barrier is barrier A (keys need every partial)
         if (tr) tr[1] = trace_now(a.trace_clk);
 
-        const double f = a.f_tab[t - a.t0];
+        const double f = f_next;
         const double alpha = a.alpha0 * f;
         double sigma = a.sigma0 * f;
         if (sigma < a.sigma_min) sigma = a.sigma_min;
@@ -597,6 +598,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
                 n_no += __popc(mn);
             }
             __syncwarp();
+            if (tr) tr[7] = trace_now(a.trace_clk);
             if (lane == 0) {
                 s_nup[(t + 1) & 1] = n_up;
                 // first rows of the next pass into the ring (none after the
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         __syncthreads();   // (B) lists, ring issue, sparse sums of t+1
         if (tr) tr[5] = trace_now(a.trace_clk);
         if (s_abort) break;
+        if (t + 1 < a.t1) f_next = a.f_tab[t + 1 - a.t0];
         scatter(t + 1);
         __syncthreads();   // (C) x_{t+1} in xs
 #pragma unroll

@@ -153,11 +153,15 @@ def test_tier_c3_late_window_equals_kernel4(som, monkeypatch):
     assert np.array_equal(out["0"][1], out["1"][1])
 
 
-def test_tier_handover_to_kernel4(som, monkeypatch):
-    """AUTO with SOM_TRAIN_TIER=1: kernel 10 while the neighbourhood covers
-    the lattice, kernel 4 from the first step where it does not (kernel id
-    11, two launches): the whole schedule against the oracle."""
+@pytest.mark.parametrize("cover", ["0.4", "0.9", "0.15"])
+def test_tier_handover_to_kernel4(som, monkeypatch, cover):
+    """AUTO with SOM_TRAIN_TIER=1: kernel 10 while the cutoff disk holds at
+    least SOM_TIER_COVER of the units on average over winner positions,
+    kernel 4 from the first step where it does not (kernel id 11, two
+    launches): the whole schedule against the oracle, at the default
+    threshold and at two other split points."""
     monkeypatch.setenv("SOM_TIER_HANDOVER", "1")
+    monkeypatch.setenv("SOM_TIER_COVER", cover)
     C = bank_corpus(300, 8000, seed=91)
     X = C.dense()
     W0 = init_rows(X, 40 * 40, 91)

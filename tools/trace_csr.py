@@ -53,3 +53,8 @@ for i in range(6):
 top0 = t[:, :, 0]
 print(f"  loop-top spread per step: median {np.median(top0.max(0) - top0.min(0)):.0f} ns; "
       f"last publisher's loop-top lag {np.median(top0[last, cols] - top0.min(0)):.0f} ns")
+if k == 4:   # TMA kernel: slot 7 = neighbourhood lists done, before the ring issue
+    for name, i, j in (("h + lists", 3, 7), ("ring issue", 7, 4)):
+        dd7 = t[:, :, j] - t[:, :, i]
+        print(f"  {name:18s} median over CTAs {np.median(np.median(dd7, axis=1)):6.0f}  "
+              f"per-step max over CTAs: median {np.median(dd7.max(0)):6.0f}")
