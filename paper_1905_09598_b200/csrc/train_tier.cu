@@ -9,9 +9,10 @@
 //
 // Where a CTA's rows live (slot s of its S units, in this order):
 //   [0, ntm)           tensor memory, used as plain storage: data thread dt
-//                      (warp w = 1..12) holds float4 chunks dt + 384 j
-//                      (j < KJ) of a row as 4 KJ words of its TMEM lane
-//                      (lane quarter w % 4), column group (w - 1) / 4 (170
+//                      (warp w = 1..NDW, NDW = 12 or 16, NDT = 32 NDW
+//                      threads) holds float4 chunks dt + NDT j (j < KJ) of a
+//                      row as 4 KJ words of its TMEM lane (lane quarter
+//                      w % 4), column group (w - 1) / 4 (512 / (NDW / 4)
 //                      columns each), 4 KJ r; moved with tcgen05.ld/st (its
 //                      own path beside the shared-memory port); updated rows
 //                      are also written through to W (the sparse sums below
@@ -22,12 +23,12 @@
 //   [ntm, non)         shared memory, [row][j][dt] float4 (conflict-free);
 //   [non, S)           W in global memory (L2-resident: only these rows are
 //                      read during the launch), streamed through a ring of
-//                      RC chunks (chunk j of a row = float4 [384 j, 384 j + 384)
+//                      RC chunks (chunk j of a row = float4 [NDT j, NDT j + NDT)
 //                      = the thread's chunk j), filled by cp.async.bulk from
 //                      the control warp, full/empty mbarriers; updated rows
 //                      are written back from registers.
 // Warp 0 is the control warp (keys, exchange, neighbourhood, lists, ring
-// producer); warps 1-12 (384 threads) hold the data.  Per step t:
+// producer); warps 1..NDW hold the data.  Per step t:
 //   1. dense pass (data warps) over the rows of update(t-1), streamed rows
 //      alternating with on-chip rows so the ring keeps moving, branch-free:
 //      w' = fmaf(h, RN(x_{t-1} - w), w) (R11; x_{t-1} in registers, built
@@ -57,20 +58,28 @@ namespace som {
 
 namespace {
 
-constexpr int NDW = 12;            // data warps 1..12
-constexpr int NDT = NDW * 32;      // data threads: own the rows' elements
-constexpr int NTH = NDT + 32;      // + control warp 0
+// data warps 1..NDW: 12 (3 TMEM column groups of 170) or 16 (4 groups of
+// 128; 544 threads at <= 120 registers, chosen where a row needs <= 5 float4
+// chunks per thread: c3 22.1 vs 23.0 us/step in the full-coverage window,
+// bit-identical, tools/lib_ab.py)
+template <int NDW>
+struct TierShape {
+    static constexpr int ndt = NDW * 32;               // data threads: own the rows' elements
+    static constexpr int nth = ndt + 32;               // + control warp 0
+    static constexpr int tm_cols = 512 / (NDW / 4);    // TMEM columns per column group
+};
 constexpr int kSlots = 32;         // units per CTA (one control lane each)
 constexpr int kRingMax = 16;       // ring chunks
-constexpr int kTmCols = 170;       // TMEM columns per column group (3 groups of 512)
 constexpr int kTmMax = 8;          // TMEM rows (unrolled loops)
 constexpr int kSmMax = 4;          // shared-memory rows (unrolled loops)
 
 struct TierPlan {
     int ntm, nsm, rc;              // TMEM rows, shared-memory rows, ring chunks
+    int ndw;                       // data warps (12 or 16)
 };
 
-__device__ __forceinline__ void bar_data() { asm volatile("bar.sync 1, %0;" ::"n"(NDT) : "memory"); }
+template <int NDT>
+__device__ __forceinline__ void bar_data_n() { asm volatile("bar.sync 1, %0;" ::"n"(NDT) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
 }
@@ -181,8 +190,12 @@ __device__ __noinline__ int list_pos(const int* ci, int cnt, int k) {
     return (lo < cnt && ci[lo] == k) ? lo : -1;
 }
 
-template <int KJ>
-__global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs a, const TierPlan p) {
+template <int KJ, int NDW>
+__global__ void __launch_bounds__(TierShape<NDW>::nth, 1) som_train_tier_kernel(const TrainArgs a, const TierPlan p) {
+    constexpr int NDT = TierShape<NDW>::ndt;
+    constexpr int NTH = TierShape<NDW>::nth;
+    constexpr int kTmCols = TierShape<NDW>::tm_cols;
+    auto bar_data = [] { bar_data_n<NDT>(); };
     __shared__ double pn[kSlots][NDW];        // |w'|^2 partials of dense-pass rows
     __shared__ double sg[2][kSlots];          // speculative S of every row, [parity of the step]
     __shared__ double sgd[kSlots];            // S(x_t) of dense-pass rows
@@ -705,37 +718,42 @@ __global__ void __launch_bounds__(NTH, 1) som_train_tier_kernel(const TrainArgs 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512) : "memory");
 }
 
-constexpr size_t kTierStatic = kSlots * NDW * 8 + 4 * kSlots * 8 + 5 * kSlots * 4 + 1024 + 512;
+constexpr size_t tier_static(int ndw) { return (size_t)kSlots * ndw * 8 + 4 * kSlots * 8 + 5 * kSlots * 4 + 1024 + 512; }
 
 size_t tier_smem_bytes(int /*S*/, int kj, int dimp, int cap, const TierPlan& p) {
-    return sizeof(float4) * (size_t)NDT * ((size_t)p.rc + (size_t)p.nsm * kj) + 4 * 4 * (size_t)NDT +
-           24 * (size_t)cap +
+    const size_t ndt = 32 * (size_t)p.ndw;
+    return sizeof(float4) * ndt * ((size_t)p.rc + (size_t)p.nsm * kj) + 4 * 4 * ndt + 24 * (size_t)cap +
            8 * (size_t)((dimp >> 5) + 1) + 128;
 }
 
-template <int KJ>
+template <int KJ, int NDW>
 cudaError_t launch_tier_kj(const TrainArgs& a, const TierPlan& p, cudaStream_t st) {
     const size_t smem = tier_smem_bytes(a.S, KJ, a.dimp, a.nz_cap, p);
-    auto fn = som_train_tier_kernel<KJ>;
+    auto fn = som_train_tier_kernel<KJ, NDW>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     TrainArgs args = a;
     TierPlan pp = p;
     void* params[] = {&args, &pp};
-    return launch_persistent((const void*)fn, a, NTH, smem, params, st);
+    return launch_persistent((const void*)fn, a, TierShape<NDW>::nth, smem, params, st);
 }
 
-int tier_kj(int dimp) { return ((dimp / 4) + NDT - 1) / NDT; }
+int tier_kj(int dimp, int ndw) { return ((dimp / 4) + 32 * ndw - 1) / (32 * ndw); }
 
 bool tier_plan(int S, int dimp, int maxnnz, int max_smem_optin, TierPlan* out) {
     if (dimp % 4 != 0 || S < 1 || S > kSlots) return false;
-    const int kj = tier_kj(dimp);
-    if (kj < 4 || kj > 8) return false;
     TierPlan p{};
-    p.ntm = std::min(kTmMax, kTmCols / (4 * kj));
+    p.ndw = 16;
+    if (const char* e = std::getenv("SOM_TIER_NDW")) p.ndw = std::atoi(e) == 12 ? 12 : 16;
+    // 16 warps spill above 5 chunks per thread; below 4 the row is short enough for 12
+    if (tier_kj(dimp, p.ndw) > 5 || tier_kj(dimp, p.ndw) < 4) p.ndw = 12;
+    const int kj = tier_kj(dimp, p.ndw);
+    if (kj < 4 || kj > 8) return false;
+    const int tm_cols = 512 / (p.ndw / 4);
+    p.ntm = std::min(kTmMax, tm_cols / (4 * kj));
     p.ntm = std::max(0, std::min(p.ntm, S));
     const int cap = csr_nz_cap(maxnnz);
-    const size_t budget = (size_t)max_smem_optin - kTierStatic;
+    const size_t budget = (size_t)max_smem_optin - tier_static(p.ndw);
     int rc_min = 8, rc_max = kRingMax;
     if (const char* e = std::getenv("SOM_TIER_RING")) rc_max = std::max(2, std::min(kRingMax, std::atoi(e))), rc_min = std::min(rc_min, rc_max);
     int smax = kSmMax;
@@ -766,12 +784,19 @@ bool train_tier_supported(int S, int dim, int maxnnz, int max_smem_optin) {
 cudaError_t launch_train_tier(const TrainArgs& a, int max_smem_optin, cudaStream_t st) {
     TierPlan p;
     if (!tier_plan(a.S, a.dimp, a.nz_cap, max_smem_optin, &p)) return cudaErrorInvalidConfiguration;
-    switch (tier_kj(a.dimp)) {
-        case 4: return launch_tier_kj<4>(a, p, st);
-        case 5: return launch_tier_kj<5>(a, p, st);
-        case 6: return launch_tier_kj<6>(a, p, st);
-        case 7: return launch_tier_kj<7>(a, p, st);
-        case 8: return launch_tier_kj<8>(a, p, st);
+    if (p.ndw == 16) {
+        switch (tier_kj(a.dimp, 16)) {
+            case 4: return launch_tier_kj<4, 16>(a, p, st);
+            case 5: return launch_tier_kj<5, 16>(a, p, st);
+            default: return cudaErrorInvalidConfiguration;
+        }
+    }
+    switch (tier_kj(a.dimp, 12)) {
+        case 4: return launch_tier_kj<4, 12>(a, p, st);
+        case 5: return launch_tier_kj<5, 12>(a, p, st);
+        case 6: return launch_tier_kj<6, 12>(a, p, st);
+        case 7: return launch_tier_kj<7, 12>(a, p, st);
+        case 8: return launch_tier_kj<8, 12>(a, p, st);
         default: return cudaErrorInvalidConfiguration;
     }
 }

@@ -69,7 +69,12 @@ def _check(W, log, Wo, logo):
     (30, 30, 12000, 1000, 300, 40),     # KJ 8 (ragged last chunk: 3000 float4 = 7 x 384 + 312)
     (40, 40, 7000, 800, 300, 148),      # 1,600 units on 148 CTAs: 10-11 rows each, no streamed row
 ])
-def test_tier_matches_oracle(som, rows, cols, d, n, steps, grid):
+@pytest.mark.parametrize("ndw", ["16", "12"])
+def test_tier_matches_oracle(som, monkeypatch, rows, cols, d, n, steps, grid, ndw):
+    """KJ counts are those of 12 data warps; SOM_TIER_NDW=16 (the default
+    where a row needs 4-5 float4 chunks per thread of 16 warps) covers
+    d = 7600 ... 10000 with 16 data warps and 128-column TMEM groups."""
+    monkeypatch.setenv("SOM_TIER_NDW", ndw)
     C = bank_corpus(n, d, seed=d + n)
     X = C.dense()
     W0 = init_rows(X, rows * cols, 31)
