@@ -69,8 +69,13 @@ def _run_sharded(som, P, rows, cols, topo, X, W0, epochs, sigma0, seed, grid, t_
     return W, [np.concatenate(l) for l in logs]
 
 
-@pytest.mark.parametrize("P,grid", [(1, 16), (2, 16), (4, 8)])
-def test_neuron_sharded_training_equals_unsharded(som, P, grid):
+@pytest.mark.parametrize("P,grid,xchg", [(1, 16, "0"), (2, 16, "0"), (4, 8, "0"), (2, 16, "1"), (2, 16, "2"),
+                                         (4, 8, "2")])
+def test_neuron_sharded_training_equals_unsharded(som, monkeypatch, P, grid, xchg):
+    """Every in-GPU exchange variant (som_internal.h: 0 tagged all-gather, 1
+    atomic max + counter, 2 counter-hinted all-gather) under the cross-rank
+    mailbox level."""
+    monkeypatch.setenv("SOM_XCHG_ATOMIC", xchg)
     C = bank_corpus(300, 512, seed=41)
     X = C.dense()
     W0 = init_rows(X, 12 * 12, 41)
