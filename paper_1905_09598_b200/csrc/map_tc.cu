@@ -24,7 +24,7 @@
 // K=8 per instruction, 12 instructions per 32-wide K-block), warps 2-5 =
 // epilogue: tcgen05.ld 32 accumulator columns at a time, D in fp32, running
 // top-2 (D, u) per document row across all unit tiles of the work item.
-// Two TMEM accumulators (2 x BN columns) hold the hi.hi products and the
+// Two TMEM accumulators (2 x BN columns, per buffer) hold the hi.hi products and the
 // two small lo products separately (accuracy: see the MMA loop).  A work item is (128-document block, range
 // of unit tiles); its partial top-2 keys go to the same merge kernel as the
 // exact path.
@@ -39,14 +39,21 @@ namespace som {
 namespace {
 
 constexpr int TC_BM = 128;
-constexpr int TC_BN = 256;
+// Unit tile of 128 (3 stages of 64 KB, two accumulator buffers in TMEM: the
+// epilogue of tile i overlaps the MMAs of tile i + 1) or (SOM_TC_BN=256)
+// 256 (2 stages of 96 KB, one accumulator buffer)
+#ifndef SOM_TC_BN
+#define SOM_TC_BN 128
+#endif
+constexpr int TC_BN = SOM_TC_BN;
 constexpr int TC_BK = 32;                 // fp32 elements = 128 B = one swizzle atom row
-constexpr int TC_STAGES = 2;
+constexpr int TC_STAGES = TC_BN == 128 ? 3 : 2;
+constexpr int TC_ACC_BUFS = TC_BN == 128 ? 2 : 1;
 constexpr int TC_THREADS = 192;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;            // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;            // 32 KB
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
-constexpr uint32_t TMEM_COLS = 2 * TC_BN;                  // hh and lo accumulators
+constexpr uint32_t TMEM_COLS = 2 * TC_BN * TC_ACC_BUFS;     // hh and lo accumulators per buffer
 constexpr int TC_K = 4;                                    // candidates per document (R20b)
 
 // ------------------------------------------------------------ PTX helpers
@@ -219,14 +226,14 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
         uint32_t tile = 0;
         for (int wi = blockIdx.x; wi < work_items; wi += gridDim.x, ++tile) {
             {
-                // one tile in flight: accumulator hh (x_hi.w_hi) at column 0 and
+                // accumulator buffer `buf`: hh (x_hi.w_hi) at its column 0 and
                 // lo (x_lo.w_hi + x_hi.w_lo) at column BN, so the large
                 // accumulator takes K/8 adds instead of 3K/8 (its fp32
                 // accumulation is not round-to-nearest)
-                const uint32_t buf = 0, tph = tile & 1;
+                const uint32_t buf = tile % TC_ACC_BUFS, tph = (tile / TC_ACC_BUFS) & 1;
                 mbar_wait(&tempty[buf], tph ^ 1);
                 tc_fence_after();
-                const uint32_t acc_hh = tmem_base, acc_lo = tmem_base + TC_BN;
+                const uint32_t acc_hh = tmem_base + buf * 2 * TC_BN, acc_lo = acc_hh + TC_BN;
                 for (int kb = 0; kb < a.kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -264,10 +271,10 @@ map_tc_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < TC_K; ++j) kk[j] = ~0ull;
             {
-                const uint32_t buf = 0, tph = tile & 1;
+                const uint32_t buf = tile % TC_ACC_BUFS, tph = (tile / TC_ACC_BUFS) & 1;
                 mbar_wait(&tfull[buf], tph);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
+                const uint32_t taddr = tmem_base + buf * 2 * TC_BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
                 for (int c = 0; c < TC_BN / 32; ++c) {
                     float v[32], vl[32];
