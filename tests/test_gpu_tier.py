@@ -174,3 +174,33 @@ def test_tier_handover_to_kernel4(som, monkeypatch, cover):
     assert k == 11, k
     Wo, logo = oracle.train_online(W0, 40, 40, 1, X, 3, 0.1, 20.0, 9)
     _check(W, log, Wo, logo)
+
+
+@pytest.mark.parametrize("tier,t0", [("1", 0), ("0", 460000)])
+def test_c3_exchange_variants_identical(som, monkeypatch, tier, t0):
+    """The three in-GPU exchange variants (som_internal.h: 0 tagged
+    all-gather, 1 atomic max + arrival counter, 2 the counter-hinted
+    all-gather, the default at G = 148) on c3 windows of kernel 10 (early,
+    every unit updated) and kernel 4 (late): the same BMU log and weights
+    bit for bit."""
+    import torch
+    from synth import CONFIGS
+    cfg = CONFIGS["c3"]
+    C = bank_corpus(cfg["n"], cfg["d"], seed=301)
+    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
+    monkeypatch.setenv("SOM_TRAIN_TIER", tier)
+    m = som.SOM(50, 50, cfg["d"], 1)
+    som.som_init_random_csr(m.h, rp, ci, va, C.n, 1301)
+    W0 = m.get_weights()
+    out = {}
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("SOM_XCHG_ATOMIC", mode)
+        m.set_weights(W0)
+        log = torch.empty(1500, dtype=torch.int32, device="cuda")
+        som.som_train_online_csr(m.h, rp, ci, va, C.n, cfg["epochs"], 0.1, cfg["sigma0"], None, 1, t0, t0 + 1500, log)
+        out[mode] = (som.som_last_train_config(m.h), m.get_weights(), log.cpu().numpy())
+    m.close()
+    assert out["2"][0][0] == 148 and out["2"][0][1] == (KERNEL_TIER if tier == "1" else 4), out["2"][0]
+    for mode in ("0", "1"):
+        assert np.array_equal(out[mode][2], out["2"][2]), f"mode {mode}: BMU log differs"
+        assert np.array_equal(out[mode][1], out["2"][1]), f"mode {mode}: weights differ"

@@ -1,2 +1,1 @@
-BENCH_ONE_DEVICE=1 BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config c2 --epochs 1 --steps 1 --warmup 3 --c5-docs 400000 --c4-steps 100 --no-baseline --table3-steps 0 --batch-epochs 0 --c2-steps 0 > gpurun_out/bench_n2.log 2>&1; echo rc=$? >> gpurun_out/bench_n2.log
-BENCH_ONE_DEVICE=1 BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 1 --warmup 3 --c5-docs 400000 --c4-steps 100 --no-baseline --table3-steps 0 --batch-epochs 0 --c2-steps 0 > gpurun_out/bench_n2_c3.log 2>&1; echo rc=$? >> gpurun_out/bench_n2_c3.log
+timeout 900 python -m pytest tests/test_gpu_tier.py -q -x -k "exchange_variants or late_window" > gpurun_out/t_x.log 2>&1; echo rc=$? >> gpurun_out/t_x.log
