@@ -162,3 +162,20 @@ def test_auto_precision_and_weight_changes(som):
         c1, c2, cd = m.map(X)
     ob1, ob2, od1 = oracle.map_docs(W2, X)
     _check_all(c1, c2, cd, ob1, ob2, od1)
+
+
+def test_tc_many_work_items_per_cta(som):
+    """More (128-document block, 128-unit tile) work items than CTAs: 10,240
+    documents x 2 unit tiles = 160 items on <= 148 persistent CTAs, so CTAs
+    run several tiles and alternate the two TMEM accumulator buffers (the
+    epilogue of one tile overlapping the MMAs of the next).  Every document
+    exact."""
+    C = bank_corpus(10240, 512, seed=15)
+    X = C.dense()
+    W = _codebook(X, 16 * 16, 16)
+    with som.SOM(16, 16, 512, 1) as m:
+        m.set_weights(W)
+        b1, b2, d1, fb = _map_tc(som, m, X)
+    ob1, ob2, od1 = oracle.map_docs(W, X)
+    _check_all(b1, b2, d1, ob1, ob2, od1)
+    print(f" [fallbacks {fb}]", end="")

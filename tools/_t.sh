@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_tier.py -q -x -k "exchange_variants or late_window" > gpurun_out/t_x.log 2>&1; echo rc=$? >> gpurun_out/t_x.log
+timeout 600 python -m pytest tests/test_gpu_map_tc.py -q -x -s -k many_work > gpurun_out/t_tc2.log 2>&1; echo rc=$? >> gpurun_out/t_tc2.log

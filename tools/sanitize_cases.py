@@ -5,7 +5,7 @@ against the oracle (BMU log equal), so a run that "passes" the sanitizer
 with a wrong answer is visible.
 
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py k2
-  cases: k1 k2 k3 k4 k5 k6 k10 k10b map_exact map_sparse map_tc metrics batch sharded2"""
+  cases: k1 k2 k3 k4 k4x1 k4x2 k5 k6 k10 k10b k10w12 map_exact map_sparse map_tc map_tc2 metrics batch sharded2"""
 import os
 import sys
 import threading
@@ -81,6 +81,24 @@ elif case == "k10":
     train_case(20, 20, 7600, 600, csr=True, expect=10, grid=20)
 elif case == "k10b":
     train_case(20, 20, 6000, 600, csr=True, expect=10, grid=16)
+elif case == "k4x1":   # kernel 4 with the atomic-max exchange (G = 100 >= 96)
+    train_case(16, 16, 2048, 300, mode=som.SOM_TRAIN_W_GLOBAL, csr=True, expect=4, grid=100,
+               env={"SOM_XCHG_ATOMIC": "1"})
+elif case == "k4x2":   # kernel 4 with the counter-hinted all-gather (the default from 96 CTAs)
+    train_case(16, 16, 2048, 300, mode=som.SOM_TRAIN_W_GLOBAL, csr=True, expect=4, grid=100)
+elif case == "k10w12":   # kernel 10 with 12 data warps on a row 16 warps would take
+    train_case(20, 20, 7600, 600, csr=True, expect=10, grid=20, env={"SOM_TIER_NDW": "12"})
+elif case == "map_tc2":   # > 148 work items: CTAs alternate the two TMEM accumulator buffers
+    C = bank_corpus(10240, 512, seed=15)
+    X = C.dense()
+    W = init_rows(X, 16 * 16, 16)
+    with som.SOM(16, 16, 512, 1) as m:
+        m.set_weights(W)
+        m.set_map_precision(som.SOM_MAP_3XTF32)
+        b1, b2, d1 = m.map(X)
+    ob1, ob2, od1 = oracle.map_docs(W, X)
+    assert np.array_equal(b1, ob1) and np.array_equal(b2, ob2)
+    print(f"{case}: {C.n} docs, bmu1/bmu2 = oracle on every document")
 elif case == "map_exact":
     map_case(som.SOM_MAP_EXACT_F64, False)
 elif case == "map_sparse":
