@@ -130,3 +130,68 @@ def test_doc_sharded_mapping_equals_unsharded(som):
     assert np.array_equal(np.concatenate([p[0] for p in parts]), b1)
     assert np.array_equal(np.concatenate([p[1] for p in parts]), b2)
     assert np.array_equal(np.concatenate([p[2] for p in parts]), d1)
+
+
+@pytest.mark.parametrize("tier,grid", [("1", 16), ("0", 16), ("1", 24)])
+def test_neuron_sharded_csr_kernels(som, monkeypatch, tier, grid):
+    """The kernels the sharded c3 bench step runs (CSR input): kernel 10
+    (SOM_TRAIN_TIER=1, TMEM + shared-memory rows + the streamed ring) and
+    kernel 4 under the cross-rank mailbox level, P = 2 ranks on one device:
+    BMU log and weights identical to the unsharded run and the log to the
+    oracle's."""
+    import torch
+
+    from paper_1905_09598_b200.dist import ShardedSOM
+    monkeypatch.setenv("SOM_TRAIN_TIER", tier)
+    monkeypatch.setenv("SOM_TIER_HANDOVER", "0")
+    # ranks emulated on one device: no persisting-L2 window (setting the
+    # device-wide set-aside can wait behind a peer's spinning grid; each
+    # rank owns its device in a real run)
+    monkeypatch.setenv("SOM_NO_L2_WINDOW", "1")
+    rows, cols, d, P, T = 20, 20, 7600, 2, 300
+    C = bank_corpus(600, d, seed=44)
+    X = C.dense()
+    W0 = init_rows(X, rows * cols, 44)
+    rp, ci, va = (torch.from_numpy(a).cuda() for a in (C.indptr, C.indices, C.data))
+    ranks = [ShardedSOM(rows, cols, d, 1, r, P, device=0, defer_peers=True) for r in range(P)]
+    boxes = [s.mailbox_ptr() for s in ranks]
+    for s in ranks:
+        s.set_peers(boxes)
+        som.som_set_train_grid(s.h, grid)
+        s.set_weights(W0)
+    logs, kernels, errors = [None] * P, [None] * P, []
+    bar = threading.Barrier(P)
+
+    def work(r):
+        try:
+            log = torch.empty(T, dtype=torch.int32, device="cuda")
+            bar.wait()
+            som.som_train_online_csr(ranks[r].h, rp, ci, va, C.n, 1, 0.1, 10.0, None, 7, 0, T, log)
+            bar.wait()
+            logs[r] = log.cpu().numpy()
+            kernels[r] = som.som_last_train_config(ranks[r].h)[1]
+        except Exception as e:
+            errors.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    W = np.zeros((rows * cols, d), np.float32)
+    for s in ranks:
+        som.som_get_weights(s.h, W)
+        s.close()
+    assert kernels[0] == (10 if tier == "1" else 4), kernels
+    with som.SOM(rows, cols, d, 1) as m:
+        m.set_weights(W0)
+        ref = np.empty(T, np.int32)
+        m.train_online_csr(C.indptr, C.indices, C.data, C.n, 1, alpha0=0.1, sigma0=10.0, seed=7, t_end=T, bmu_log=ref)
+        Wref = m.get_weights()
+    for r in range(P):
+        assert np.array_equal(logs[r], ref), f"rank {r} BMU log differs"
+    assert np.array_equal(W, Wref)
+    _, logo = oracle.train_online(W0, rows, cols, 1, X, 1, 0.1, 10.0, 7, t_end=T)
+    assert np.array_equal(ref, logo)

@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_map_tc.py -q -x -s -k many_work > gpurun_out/t_tc2.log 2>&1; echo rc=$? >> gpurun_out/t_tc2.log
+for i in 1 2 3; do timeout 900 python -m pytest tests/test_gpu_sharded.py -q -x -k csr_kernels > gpurun_out/t_sh$i.log 2>&1; echo rc=$? >> gpurun_out/t_sh$i.log; done
