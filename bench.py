@@ -72,6 +72,9 @@ def dist_env():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if os.environ.get("BENCH_ONE_DEVICE") == "1":   # test hook: every rank on cuda:0 (multi-rank plumbing check)
         local = 0
+        # no persisting-L2 window: its device-wide set-aside can wait behind
+        # a peer rank's spinning grid on the shared device
+        os.environ.setdefault("SOM_NO_L2_WINDOW", "1")
     return rank, world, local
 
 
