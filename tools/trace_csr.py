@@ -58,3 +58,15 @@ if k == 4:   # TMA kernel: slot 7 = neighbourhood lists done, before the ring is
         dd7 = t[:, :, j] - t[:, :, i]
         print(f"  {name:18s} median over CTAs {np.median(np.median(dd7, axis=1)):6.0f}  "
               f"per-step max over CTAs: median {np.median(dd7.max(0)):6.0f}")
+# CTAs that updated rows this step (dense pass > 600 ticks) vs the others
+dp = t[:, :, 1] - t[:, :, 0]
+upd = dp > 600
+if upd.any():
+    print(f"  steps x CTAs with a dense pass: {upd.mean() * 100:.1f} %")
+    for i in range(6):
+        dd6 = t[:, :, i + 1] - t[:, :, i]
+        print(f"    {names[i]:18s} updating CTAs median {np.median(dd6[upd]):7.0f}   others {np.median(dd6[~upd]):7.0f}")
+    if k == 4:
+        for name, i, j in (("h + lists", 3, 7), ("ring issue", 7, 4)):
+            dd7 = t[:, :, j] - t[:, :, i]
+            print(f"    {name:18s} updating CTAs median {np.median(dd7[upd]):7.0f}   others {np.median(dd7[~upd]):7.0f}")
