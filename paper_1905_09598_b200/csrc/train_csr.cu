@@ -571,6 +571,10 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             best = warp_min_u64(best);
             if (tr) tr[2] = trace_now(a.trace_clk);
             xchg_publish(a, best, t, b, lane);
+            // the data warps start their speculative sums only now: run
+            // beside the keys above they slowed them down (shared
+            // sub-partition and conversion pipe) on the step's critical path
+            asm volatile("bar.arrive 3, %0;" ::"n"(NT) : "memory");
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
             if (stop && lane == 0) s_abort = 1;
@@ -615,9 +619,11 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             }
             if (tr) tr[4] = trace_now(a.trace_clk);
         } else {
-            // warps 1-15: list of x_{t+2}, bounds of x_{t+3}, and the
-            // speculative sparse sums of step t+1 (skipped when the radius
-            // covers the whole lattice: every unit takes the dense pass)
+            // warps 1-15, once warp 0 has published: list of x_{t+2}, bounds
+            // of x_{t+3}, and the speculative sparse sums of step t+1
+            // (skipped when the radius covers the whole lattice: every unit
+            // takes the dense pass)
+            asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");
             stage_list(t + 2, threadIdx.x - 32, NT - 32);
             if (warp == 1 && lane == 0 && t + 3 < a.t1) bounds(t + 3);
             if (!(r2 >= a.g2max)) sparse_sums(t + 1, 1, NW - 1);

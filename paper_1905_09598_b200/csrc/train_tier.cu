@@ -593,6 +593,9 @@ __global__ void __launch_bounds__(TierShape<NDW>::nth, 1) som_train_tier_kernel(
             best = warp_min_u64(best);
             if (tr) tr[3] = trace_now(a.trace_clk);
             xchg_publish(a, best, t, b, lane);
+            // the data warps start 2' only now: beside the keys above it
+            // slowed them down on the step's critical path
+            asm volatile("bar.arrive 3, %0;" ::"n"(NTH) : "memory");
             int stop = 0;
             const unsigned long long gmin = xchg_wait(a, t, b, lane, &stop);
             if (tr) tr[4] = trace_now(a.trace_clk);
@@ -649,7 +652,8 @@ __global__ void __launch_bounds__(TierShape<NDW>::nth, 1) som_train_tier_kernel(
             // ---- 2'. data warps: list of x_{t+2}, bounds of x_{t+3}, bitmap
             // of x_{t+1}, speculative S(x_{t+1}) of every unit (skipped when
             // the radius covers the whole lattice: every unit then takes the
-            // dense pass)
+            // dense pass), once the control warp has published
+            asm volatile("bar.sync 3, %0;" ::"n"(NTH) : "memory");
             stage_list(t + 2);
             if (dt == 0 && t + 3 < a.t1) bounds(t + 3);
             uint32_t mn = 0u;
