@@ -163,6 +163,9 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
             key = __shfl_sync(0xffffffffu, key, 0);
 
             xchg_publish(a, key, t, b, lane);
+            // warps 1-15 start the neighbourhood table only now: beside the
+            // key above it slowed it down on the step's critical path
+            asm volatile("bar.arrive 3, %0;" ::"n"(NT) : "memory");
             TRACE(3);
             shift_x(t + 1);                       // hidden behind the poll
             int stop = 0;
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
             }
             TRACE(5);
         } else {
+            asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");   // warp 0 has published
             shift_x(t + 1);
             // neighbourhood table of step t (schedule R1-R3, kernel R4, cutoff
             // R5), built while warp 0 waits on the exchange
