@@ -30,7 +30,7 @@ constexpr int NW = kTrainWarps;
 template <int SMAX, int KJ>
 __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a) {
     __shared__ double part[NW][SMAX];        // per-warp partial distance of each unit
-    __shared__ int s_c;                      // winner of the current step
+    __shared__ int s_c, s_ic, s_jc;          // winner of the current step, its lattice row / column
     __shared__ int s_abort;
     extern __shared__ __align__(16) float xring[];   // [3][dimp] x ring, then the h table
 
@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
             TRACE(4);
             if (lane == 0) {
                 s_c = c;
+                s_ic = c / a.cols;
+                s_jc = c - s_ic * a.cols;
                 if (stop) s_abort = 1;
                 if (b == 0 && a.bmu_log) a.bmu_log[t - a.t0] = c;
             }
@@ -203,8 +205,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         if (s_abort) break;
         {
             // every thread looks up h for its CTA's units (exact g2 offsets)
-            const int c = s_c;
-            const int ic = c / a.cols, jc = c - ic * a.cols;
+            const int ic = s_ic, jc = s_jc;
 #pragma unroll
             for (int s = 0; s < SMAX; ++s) {
                 const int di = abs(ui[s] - ic);
