@@ -150,16 +150,30 @@ __global__ void __launch_bounds__(NT, 1) som_train_reg_kernel(const TrainArgs a)
         TRACE(2);
 
         if (warp == 0) {
-            // lane s sums its unit's 16 warp partials (fixed order), keys, min
             unsigned long long key = ~0ull;
-            if (lane < SMAX && lane < Sb) {
-                double tot = 0.0;
+            if constexpr (SMAX * 8 <= 32 && NW == 16) {
+                // 8 lanes per unit, two warp partials each, a 3-level
+                // butterfly (fixed order), then the min over the units
+                const int su = lane >> 3, pi = (lane & 7) * 2;
+                double v = 0.0;
+                if (su < SMAX) v = part[pi][su] + part[pi + 1][su];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                if ((lane & 7) == 0 && su < SMAX && su < Sb) key = make_key((float)v, global_unit(a, b + su * G));
 #pragma unroll
-                for (int w8 = 0; w8 < NW; ++w8) tot += part[w8][lane];
-                key = make_key((float)tot, global_unit(a, b + lane * G));
+                for (int o = 8; o < 8 * SMAX; o <<= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
+            } else {
+                // lane s sums its unit's warp partials (fixed order), keys, min
+                if (lane < SMAX && lane < Sb) {
+                    double tot = 0.0;
+#pragma unroll
+                    for (int w8 = 0; w8 < NW; ++w8) tot += part[w8][lane];
+                    key = make_key((float)tot, global_unit(a, b + lane * G));
+                }
+#pragma unroll
+                for (int o = SMAX / 2; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
             }
-#pragma unroll
-            for (int o = SMAX / 2; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
             key = __shfl_sync(0xffffffffu, key, 0);
 
             xchg_publish(a, key, t, b, lane);
