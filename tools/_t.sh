@@ -1,1 +1,2 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_spec.py tests/test_gpu_sharded.py tests/test_gpu_trajectory_pins.py tests/test_gpu_sampling.py tests/test_gpu_zero_rows.py tests/test_gpu_nccl.py -q -x > gpurun_out/t_k2.log 2>&1; echo rc=$? >> gpurun_out/t_k2.log
+# scratch driver for gpurun calls (the last command run on the GPU box)
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
