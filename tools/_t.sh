@@ -1,3 +1,3 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-SOM_TIER_HANDOVER=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:som_train_tier -c 1 -o gpurun_out/k10_early_v2 python tools/c3_window.py 0 1000 > gpurun_out/ncu_k10.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:som_train_reg -c 1 -o gpurun_out/k2_c2 python tools/trace_train.py c2 128 20000 0 > gpurun_out/ncu_k2.log 2>&1
+for w in "320000 3000" "350000 3000" "450000 3000"; do for L in A R A R; do SOM_TRAIN_TIER=0 SOM_LIB=ab/libsom_$L.so python tools/lib_ab.py $w; done; done > gpurun_out/ab_k4c.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_train_csr.py tests/test_gpu_tier.py tests/test_gpu_sharded.py tests/test_gpu_trajectory_pins.py tests/test_gpu_zero_rows.py tests/test_gpu_sampling.py -q -x > gpurun_out/t_k4.log 2>&1; echo rc=$? >> gpurun_out/t_k4.log
