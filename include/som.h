@@ -40,8 +40,12 @@
  *    (documents per CTA), SOM_NO_TMA_RING (1: register-pipelined streamed
  *    training kernel), SOM_NO_L2_WINDOW (1: no persisting L2 window),
  *    SOM_POLL_NS (back-off between exchange polls), SOM_TRACE_CLOCK (1:
- *    som_set_trace records SM cycles).  Every variant they select is
- *    covered by the parity tests.
+ *    som_set_trace records SM cycles), SOM_XCHG_ATOMIC (in-GPU winner
+ *    exchange: 0 tagged all-gather, 1 atomic max + arrival counter, 2 the
+ *    all-gather read once a relaxed arrival counter is complete; default 2
+ *    from 96 CTAs, else 0), SOM_TIER_NDW (12|16: kernel 10's data warps),
+ *    SOM_TIER_COVER (kernel 10 -> 4 hand-over coverage, default 0.4).
+ *    Every variant they select is covered by the parity tests.
  */
 #ifndef SOM_H
 #define SOM_H
@@ -199,8 +203,9 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * Kernel 10 = CSR input (or sparse dense rows, converted on the device) in
  * AUTO mode where W does not fit the SMs' shared memory: the map held in
  * tensor memory and shared memory, the rest streamed through a TMA ring
- * (train_tier.cu).  It runs while the neighbourhood covers the whole
- * lattice and kernel 4 after (kernel 11 = both, two launches in one call;
+ * (train_tier.cu).  It runs while the cutoff disk holds >= 40 % of the
+ * units on average over winner positions and kernel 4 after (kernel 11 =
+ * both, two launches in one call;
  * SOM_TIER_HANDOVER=0 keeps kernel 10, SOM_TRAIN_TIER=0 selects kernel 4
  * throughout).
  * All follow the same arithmetic contract (R9-R11). */
