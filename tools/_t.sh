@@ -1,3 +1,2 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
+SOM_TRACE_CLOCK=1 python tools/trace_tier.py 0 2000 1 > gpurun_out/trace_k10b.log 2>&1
