@@ -1,2 +1,4 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-for w in "0 3000" "280000 3000"; do for n in 16 15 16 15; do echo -n "ndw=$n "; SOM_TIER_NDW=$n python tools/lib_ab.py $w; done; done > gpurun_out/ab_ndw15.log 2>&1
+python tools/prof_c4.py 200 1 > gpurun_out/c4.log 2>&1
+python tools/prof_c4.py 200 0 >> gpurun_out/c4.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:som_train -c 1 -o gpurun_out/k4_c4 python tools/prof_c4.py 100 1 > gpurun_out/ncu_c4.log 2>&1
