@@ -71,6 +71,47 @@ void build_unit_tab(int rows, int cols, int topo, int rank, int world, int NL, i
     }
 }
 
+// Fraction of the units inside the cutoff disk at step t, averaged over 64
+// sampled winner positions (non-increasing in t): the hand-over criterion
+// of the two-kernel schedules (kernels 11 and 12).
+double mean_cover(const som_ctx* h, const som_schedule& sd, int64_t T, double sigma0, double ln_inv_eps, int64_t t) {
+    double f;
+    fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
+    const double sigma = std::max(sd.sigma_min, sigma0 * f);
+    const double r2 = 2.0 * sigma * sigma * ln_inv_eps;
+    const int Nm = h->rows * h->cols;
+    const int stride = std::max(1, Nm / 64);
+    int64_t cnt = 0, pos = 0;
+    for (int c = stride / 2; c < Nm; c += stride, ++pos) {
+        const int ic = c / h->cols, jc = c - ic * h->cols;
+        for (int i = 0; i < h->rows; ++i) {
+            const double di = (double)(i - ic);
+            for (int j = 0; j < h->cols; ++j) {
+                double g2;
+                if (h->topo == 0) {
+                    const double dj = (double)(j - jc);
+                    g2 = di * di + dj * dj;
+                } else {
+                    const double dx2 = (double)(2 * (j - jc) + ((i & 1) - (ic & 1)));
+                    g2 = 0.25 * dx2 * dx2 + 0.75 * di * di;
+                }
+                cnt += g2 <= r2;
+            }
+        }
+    }
+    return (double)cnt / ((double)pos * Nm);
+}
+
+// first t in [lo, hi) whose mean coverage is below thr (hi if none)
+int64_t first_below(const som_ctx* h, const som_schedule& sd, int64_t T, double sigma0, double ln_inv_eps, double thr,
+                    int64_t lo, int64_t hi) {
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (mean_cover(h, sd, T, sigma0, ln_inv_eps, mid) >= thr) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, int32_t epochs, double alpha0,
                       double sigma0, const som_schedule& sd, uint64_t seed, int64_t t_begin, int64_t t_end,
                       int32_t* bmu_log) {
@@ -338,43 +379,40 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         if (const char* e = std::getenv("SOM_TIER_HANDOVER")) handover = std::atoi(e) != 0;
         double thr = 0.4;
         if (const char* e = std::getenv("SOM_TIER_COVER")) thr = std::atof(e);
-        if (handover) {
-            const int Nm = h->rows * h->cols;
-            const int stride = std::max(1, Nm / 64);
-            auto mean_cover = [&](int64_t t) {
-                double f;
-                fill_decay(&f, t, t + 1, T, sd.kind, sd.k);
-                const double sigma = std::max(sd.sigma_min, sigma0 * f);
-                const double r2 = 2.0 * sigma * sigma * a.ln_inv_eps;
-                int64_t cnt = 0, pos = 0;
-                for (int c = stride / 2; c < Nm; c += stride, ++pos) {
-                    const int ic = c / h->cols, jc = c - ic * h->cols;
-                    for (int i = 0; i < h->rows; ++i) {
-                        const double di = (double)(i - ic);
-                        for (int j = 0; j < h->cols; ++j) {
-                            double g2;
-                            if (h->topo == 0) {
-                                const double dj = (double)(j - jc);
-                                g2 = di * di + dj * dj;
-                            } else {
-                                const double dx2 = (double)(2 * (j - jc) + ((i & 1) - (ic & 1)));
-                                g2 = 0.25 * dx2 * dx2 + 0.75 * di * di;
-                            }
-                            cnt += g2 <= r2;
-                        }
-                    }
+        if (handover) t_tier = first_below(h, sd, T, sigma0, a.ln_inv_eps, thr, t_begin, t_end);
+    }
+    // kernel 3 then kernel 4 (kernel 12): CSR rows too long for kernel 4's
+    // TMA row ring (> 6 float4 per thread: c4, d = 20,000) run the dense
+    // pipelined kernel while most units update every step (it streams all
+    // of W once per step at ~94 % of HBM, kernel 4's register ring reaches
+    // ~71 % on the same full-coverage steps), then kernel 4 (sparse
+    // distances: only the updated rows move).  Exact t-range split; needs
+    // the dense rows (the caller's, or densified when the device has room).
+    // SOM_DENSE_COVER: mean-coverage threshold of the hand-over (default
+    // 0.6; 0 = kernel 4 throughout).
+    int64_t t_dense = t_begin;
+    const float* xdense = nullptr;
+    if (use_csr && !use_tier && a.cutoff_on && h->world == 1 && h->train_mode == SOM_TRAIN_AUTO &&
+        ((a.dimp / 4) + kTrainThreads - 1) / kTrainThreads > 6 && train_glb_supported(a.S, h->dim)) {
+        double thr = 0.6;
+        if (const char* e = std::getenv("SOM_DENSE_COVER")) thr = std::atof(e);
+        if (thr > 0.0) t_dense = first_below(h, sd, T, sigma0, a.ln_inv_eps, thr, t_begin, t_end);
+        if (t_dense > t_begin) {
+            if (Xd) {
+                xdense = (const float*)Xd;
+            } else {
+                size_t fr = 0, tot = 0;
+                const size_t need = sizeof(float) * (size_t)n * h->dim;
+                if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && (h->dense.cap >= need || need + ((size_t)1 << 30) <= fr)) {
+                    CK(h->dense.ensure(need, h->stream));
+                    CK(launch_densify(csr->rowptr, csr->col, csr->val, 0, n, h->dim, (float*)h->dense.p, h->stream));
+                    xdense = (const float*)h->dense.p;
                 }
-                return (double)cnt / ((double)pos * Nm);
-            };
-            int64_t lo = t_begin, hi = t_end;   // first t in [lo, hi) below the threshold (non-increasing in t)
-            while (lo < hi) {
-                const int64_t mid = lo + (hi - lo) / 2;
-                if (mean_cover(mid) >= thr) lo = mid + 1; else hi = mid;
             }
-            t_tier = lo;
+            if (!xdense) t_dense = t_begin;
         }
     }
-    int64_t t_split = t_begin;   // hybrid: kernel 6 on [t_begin, t_split), kernel 2 after
+    int64_t t_split = t_begin;   // hybrid: kernel 6 on [t_split), kernel 2 after
     int G6 = 0;
     if (use_reg && spec_mode == 2 && h->train_mode == SOM_TRAIN_AUTO && h->train_grid == 0 && h->world == 1 &&
         (int64_t)a.S * h->dim >= 8192) {
@@ -498,7 +536,29 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
             if (t_tier > t_begin) launches = 2;
         }
     }
-    else if (use_csr) CK(launch_train_csr(a, h->stream));
+    else if (use_csr) {
+        if (t_dense > t_begin) {
+            TrainArgs a3 = a;
+            a3.X = xdense;
+            a3.x_vec4 = 1;
+            a3.t1 = t_dense;
+            CK(launch_train_glb(a3, h->stream));
+            if (t_dense < t_end) {
+                // kernel 4 from the hand-over step (fresh exchange slots; the abort flag stays)
+                CK(cudaMemsetAsync(h->xchg.p, 0, sizeof(unsigned long long) * xwords, h->stream));
+                TrainArgs a4 = a;
+                a4.t0 = t_dense;
+                a4.f_tab = a.f_tab + (t_dense - t_begin);
+                if (a4.bmu_log) a4.bmu_log = a.bmu_log + (t_dense - t_begin);
+                a4.trace = nullptr;
+                a4.trace_steps = 0;
+                CK(launch_train_csr(a4, h->stream));
+                launches = 2;
+            }
+        } else {
+            CK(launch_train_csr(a, h->stream));
+        }
+    }
     else if (use_glb) CK(launch_train_glb(a, h->stream));
     else CK(launch_train(a, smem, h->stream));
     CK(cudaEventRecord(h->ev1, h->stream));
@@ -507,7 +567,7 @@ som_status train_impl(som_ctx* h, const void* Xd, const CsrIn* csr, int64_t n, i
         cudaGetLastError();
     }
     h->last_grid = a.G;
-    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_tier ? (t_tier >= t_end ? 10 : t_tier > t_begin ? 11 : 4) : use_csr ? 4 : use_glb ? 3 : (a.w_smem ? 1 : 0);
+    h->last_kernel = use_small ? 5 : use_spec ? 6 : G6 > 0 ? (t_split < t_end ? 7 : 6) : use_reg ? 2 : use_tier ? (t_tier >= t_end ? 10 : t_tier > t_begin ? 11 : 4) : use_csr ? (t_dense >= t_end ? 3 : t_dense > t_begin ? 12 : 4) : use_glb ? 3 : (a.w_smem ? 1 : 0);
     if (bmu_log && !log_dev)
         CK(cudaMemcpyAsync(bmu_log, h->log.p, sizeof(int32_t) * (size_t)steps, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

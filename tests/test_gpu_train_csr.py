@@ -154,3 +154,21 @@ def test_csr_validation(som, defect):
         with pytest.raises(som.SomError):
             som.som_map_csr(m.h, indptr, col, val, C.n, b1)
         assert np.array_equal(m.get_weights(), W0)
+
+
+@pytest.mark.parametrize("cover,expect", [("0.6", 12), ("0", 4), ("1.01", 4)])
+def test_dense_then_sparse_kernel12(som, monkeypatch, cover, expect):
+    """AUTO with rows too long for kernel 4's TMA ring (d = 13,000: 7 float4
+    per thread): the dense pipelined kernel 3 while the cutoff disk holds >=
+    SOM_DENSE_COVER of the units on average, then kernel 4 (kernel id 12,
+    two launches; the CSR rows densified on the device), against the oracle
+    over the whole schedule; SOM_DENSE_COVER=0 / > 1 keep kernel 4
+    throughout."""
+    monkeypatch.setenv("SOM_DENSE_COVER", cover)
+    C = bank_corpus(200, 13000, seed=213)
+    X = C.dense()
+    W0 = init_rows(X, 12 * 12, 213)
+    W, log, kernel = _train_csr(som, 12, 12, 1, C, W0, 2, 0.1, 6.0, 9, mode=0, grid=16)
+    assert kernel == expect, kernel
+    Wo, logo = oracle.train_online(W0, 12, 12, 1, X, 2, 0.1, 6.0, 9)
+    _check(W, log, Wo, logo)

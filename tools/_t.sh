@@ -1,2 +1,3 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-timeout 900 python tools/sweep_tier_plan.py 3000 > gpurun_out/sweep_plan.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
