@@ -44,7 +44,9 @@
  *    exchange: 0 tagged all-gather, 1 atomic max + arrival counter, 2 the
  *    all-gather read once a relaxed arrival counter is complete; default 2
  *    from 96 CTAs, else 0), SOM_TIER_NDW (12|16: kernel 10's data warps),
- *    SOM_TIER_COVER (kernel 10 -> 4 hand-over coverage, default 0.4).
+ *    SOM_TIER_COVER (kernel 10 -> 4 hand-over coverage, default 0.4),
+ *    SOM_DENSE_COVER (kernel 3 -> 4 hand-over coverage of kernel 12,
+ *    default 0.6; 0 = kernel 4 throughout).
  *    Every variant they select is covered by the parity tests.
  */
 #ifndef SOM_H
@@ -207,7 +209,11 @@ som_status som_set_train_grid(som_ctx *h, int32_t grid);
  * units on average over winner positions and kernel 4 after (kernel 11 =
  * both, two launches in one call;
  * SOM_TIER_HANDOVER=0 keeps kernel 10, SOM_TRAIN_TIER=0 selects kernel 4
- * throughout).
+ * throughout).  Kernel 12 = CSR rows too long for kernel 4's TMA row ring
+ * (> 6 float4 per thread, e.g. d = 20,000) on one GPU in AUTO mode: the
+ * dense pipelined kernel 3 on the dense rows (densified on the device when
+ * it has room) while the cutoff disk holds >= 60 % of the units on average
+ * (SOM_DENSE_COVER), then kernel 4 (two launches in one call).
  * All follow the same arithmetic contract (R9-R11). */
 som_status som_last_train_config(som_ctx *h, int32_t *grid, int32_t *kernel);
 
