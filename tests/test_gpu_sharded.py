@@ -132,7 +132,7 @@ def test_doc_sharded_mapping_equals_unsharded(som):
     assert np.array_equal(np.concatenate([p[2] for p in parts]), d1)
 
 
-@pytest.mark.parametrize("tier,grid", [("1", 16), ("0", 16), ("1", 24)])
+@pytest.mark.parametrize("tier,grid", [("1", 16), ("0", 16), ("1", 24), ("11", 16)])
 def test_neuron_sharded_csr_kernels(som, monkeypatch, tier, grid):
     """The kernels the sharded c3 bench step runs (CSR input): kernel 10
     (SOM_TRAIN_TIER=1, TMEM + shared-memory rows + the streamed ring) and
@@ -142,13 +142,15 @@ def test_neuron_sharded_csr_kernels(som, monkeypatch, tier, grid):
     import torch
 
     from paper_1905_09598_b200.dist import ShardedSOM
-    monkeypatch.setenv("SOM_TRAIN_TIER", tier)
-    monkeypatch.setenv("SOM_TIER_HANDOVER", "0")
+    # tier "11": kernel 10 then kernel 4 inside one call (the hand-over of
+    # the sharded c3 bench step), over the whole schedule
+    monkeypatch.setenv("SOM_TRAIN_TIER", "1" if tier == "11" else tier)
+    monkeypatch.setenv("SOM_TIER_HANDOVER", "1" if tier == "11" else "0")
     # ranks emulated on one device: no persisting-L2 window (setting the
     # device-wide set-aside can wait behind a peer's spinning grid; each
     # rank owns its device in a real run)
     monkeypatch.setenv("SOM_NO_L2_WINDOW", "1")
-    rows, cols, d, P, T = 20, 20, 7600, 2, 300
+    rows, cols, d, P, T = 20, 20, 7600, 2, (600 if tier == "11" else 300)
     C = bank_corpus(600, d, seed=44)
     X = C.dense()
     W0 = init_rows(X, rows * cols, 44)
@@ -184,7 +186,7 @@ def test_neuron_sharded_csr_kernels(som, monkeypatch, tier, grid):
     for s in ranks:
         som.som_get_weights(s.h, W)
         s.close()
-    assert kernels[0] == (10 if tier == "1" else 4), kernels
+    assert kernels[0] == {"1": 10, "0": 4, "11": 11}[tier], kernels
     with som.SOM(rows, cols, d, 1) as m:
         m.set_weights(W0)
         ref = np.empty(T, np.int32)

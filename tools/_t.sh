@@ -1,3 +1,2 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
+for i in 1 2; do timeout 900 python -m pytest tests/test_gpu_sharded.py -q -x -k csr_kernels > gpurun_out/t_sh$i.log 2>&1; echo rc=$? >> gpurun_out/t_sh$i.log; done
