@@ -1,2 +1,2 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-BENCH_ONE_DEVICE=1 BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config c2 --epochs 1 --steps 1 --warmup 3 --c5-docs 400000 --c4-steps 100 --no-baseline --table3-steps 0 --batch-epochs 0 --c2-steps 0 > gpurun_out/bench_n2.log 2>&1; echo rc=$? >> gpurun_out/bench_n2.log
+for w in "0 3000" "280000 3000"; do for L in A B A B; do SOM_LIB=ab/libsom_$L.so python tools/lib_ab.py $w; done; done > gpurun_out/ab_k10g.log 2>&1
