@@ -423,12 +423,12 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
         }
     };
     // sparse sums of slots [s_begin, Sb) step s_step, list of x_t, warp-wide
-    auto sparse_sums = [&](int64_t t, int w_first, int w_count) {
+    auto sparse_sums = [&](int64_t t, int w_index, int w_count) {
         if (t >= a.t1) return;
         const int cnt = (int)(nb[t % 3][1] - nb[t % 3][0]);
         const int* li = nzi + (size_t)(t & 1) * cap;
         const float* lv = nzv + (size_t)(t & 1) * cap;
-        for (int s = warp - w_first; s < Sb; s += w_count) {
+        for (int s = w_index; s < Sb; s += w_count) {
             const float* row = a.W + (int64_t)uid[s] * a.dimp;
             double acc = 0.0;
             for (int p = lane; p < cnt; p += 32) {
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
     __syncthreads();
     if (threadIdx.x == 0 && a.t0 + 2 < a.t1) bounds(a.t0 + 2);
     scatter(a.t0);
-    sparse_sums(a.t0, 0, NW);
+    sparse_sums(a.t0, warp, NW);
     for (int s = threadIdx.x; s < Sb; s += NT) {
         double tot = 0.0;
 #pragma unroll
@@ -624,9 +624,15 @@ __global__ void __launch_bounds__(NT, 1) som_train_csr_tma_kernel(const TrainArg
             // (skipped when the radius covers the whole lattice: every unit
             // takes the dense pass)
             asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");
-            stage_list(t + 2, threadIdx.x - 32, NT - 32);
-            if (warp == 1 && lane == 0 && t + 3 < a.t1) bounds(t + 3);
-            if (!(r2 >= a.g2max)) sparse_sums(t + 1, 1, NW - 1);
+            // only the 12 warps off warp 0's sub-partition (warp % 4 != 0):
+            // warps 4, 8, 12 stay idle so the exchange poll keeps its issue
+            // slot and pipes
+            if ((warp & 3) != 0) {
+                const int hid = warp - 1 - (warp >> 2);   // 0..11
+                stage_list(t + 2, hid * 32 + lane, 12 * 32);
+                if (warp == 1 && lane == 0 && t + 3 < a.t1) bounds(t + 3);
+                if (!(r2 >= a.g2max)) sparse_sums(t + 1, hid, 12);
+            }
         }
         cp_async_wait_all();
         __syncthreads();   // (B) lists, ring issue, sparse sums of t+1
