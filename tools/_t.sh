@@ -1,2 +1,4 @@
 # scratch driver for gpurun calls (the last command run on the GPU box)
-for L in A V A V; do SOM_LIB=ab/libsom_$L.so python tools/sweep_grid.py c2 20 128; done > gpurun_out/ab_c2d.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
